@@ -1,0 +1,188 @@
+/*
+ * snpb200.h -- C ABI of the B200 SNP-system step engine (libsnpb200.so).
+ *
+ * The reference (snpsim 0.1.0, pure Python + numpy) has no FFI; its plug
+ * point is the hard-coded format dispatch inside the engine:
+ *
+ *   prepare()            pkg/src/snpsim/engine.py:388-402   -> snp_engine_create
+ *   simulate_prepared()  pkg/src/snpsim/engine.py:416-461   -> snp_begin + snp_advance
+ *                                                               (snp_run = both + final read)
+ *   sv_calc()            pkg/src/snpsim/engine.py:192-236   -> snp_sv_calc
+ *   step_sparse/_ell/_compressed()
+ *                        pkg/src/snpsim/engine.py:239-355   -> snp_step
+ *   update_delays()      pkg/src/snpsim/engine.py:358-366   -> snp_update_delays
+ *   NegativeSpikes       pkg/src/snpsim/engine.py:48-54     -> SNP_ERR_NEGATIVE
+ *
+ * Every entry point takes plain HOST pointers in the reference's own array
+ * layouts (int64 counts, numpy-bool kinds, NULL = -1 padding) and sizes; the
+ * library owns all device memory.  No torch / CUDA types cross the boundary
+ * (streams are internal; one stream per engine).  An engine is not
+ * re-entrant (same contract as the reference engine).
+ *
+ * Return codes: 0 ok; SNP_ERR_NEGATIVE -> NegativeSpikes; SNP_ERR_BAD_ARG ->
+ * ValueError; SNP_ERR_CUDA / SNP_ERR_CAPACITY -> RuntimeError / MemoryError.
+ * snp_last_error() returns the thread's last message.
+ */
+#ifndef SNPB200_H
+#define SNPB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNPB200_ABI_VERSION 1
+
+enum {
+    SNP_OK = 0,
+    SNP_ERR_NEGATIVE = 1,
+    SNP_ERR_BAD_ARG = 2,
+    SNP_ERR_CUDA = 3,
+    SNP_ERR_CAPACITY = 4
+};
+
+/* matrices.py:33-45 Format (ORACLE has no device backend) */
+enum { SNP_FMT_SPARSE = 0, SNP_FMT_ELL = 1, SNP_FMT_COMPRESSED = 2 };
+
+/* COMPRESSED only: gather from in-adjacency (atomic-free, default) or the
+ * paper's Alg. 5 push with atomics over the out-adjacency. */
+enum { SNP_VARIANT_AUTO = 0, SNP_VARIANT_PULL = 1, SNP_VARIANT_PUSH = 2 };
+
+/* selection.py:21-31 */
+enum { SNP_POLICY_FIRST = 0, SNP_POLICY_SEEDED = 1 };
+
+/* engine.py:57-60 RecordLevel as bit flags; 0 = final state only
+ * (extension used by the benchmark). CONFIGS=1, CONFIGS_AND_DELAYS=3, FULL=7. */
+enum { SNP_REC_CONFIGS = 1, SNP_REC_DELAYS = 2, SNP_REC_SPIKING = 4 };
+
+/* engine.py:57-59 HaltReason */
+enum { SNP_RUNNING = 0, SNP_HALT_STEP_LIMIT = 1, SNP_HALT_NO_APPLICABLE = 2,
+       SNP_HALT_NEGATIVE = 3 };
+
+typedef struct snp_system_desc {
+    int32_t format;            /* SNP_FMT_* */
+    int32_t variant;           /* SNP_VARIANT_* */
+    int64_t q;                 /* neurons */
+    int64_t m;                 /* rules */
+    const int64_t *initial;    /* [q]   SNPSystem.initial_spikes           */
+    const int64_t *offsets;    /* [q+1] NeuronRuleMap.offsets              */
+    const int64_t *threshold;  /* [m]   RuleVector.threshold               */
+    const uint8_t *is_exact;   /* [m]   RuleVector.is_exact (numpy bool)   */
+    const int64_t *consumed;   /* [m]   RuleVector.consumed                */
+    const int64_t *produced;   /* [m]   RuleVector.produced                */
+    const int64_t *delay;      /* [m]   RuleVector.delay                   */
+    /* Transition structure.  Either the out-adjacency in CSR form
+     * (ascending targets per source), or -- when adj_offsets is NULL -- the
+     * reference matrix of the chosen format in its own layout:           */
+    const int64_t *adj_offsets;  /* [q+1] */
+    const int64_t *adj_targets;  /* [S]   */
+    const int64_t *syn_target;   /* SynapseMatrix.target [syn_rows][q] (matrices.py:100-112) */
+    int64_t syn_rows;
+    const int64_t *ell_target;   /* EllMatrix.target [ell_rows][m] (matrices.py:83-97) */
+    const int64_t *ell_amount;   /* EllMatrix.amount [ell_rows][m] */
+    int64_t ell_rows;
+    const int64_t *sparse_data;  /* SparseMatrix.data [m][q] (matrices.py:76-80) */
+    int32_t device;              /* CUDA ordinal */
+    int32_t reserved;
+} snp_system_desc;
+
+typedef struct snp_run_opts {
+    int64_t max_steps;     /* SimOptions.max_steps (>= 1) */
+    int32_t policy;        /* SNP_POLICY_* */
+    int32_t record;        /* SNP_REC_* flags */
+    uint64_t seed;         /* SeededRandom.seed mod 2^64 */
+    int64_t chunk;         /* steps per device loop segment (0 = auto) */
+    int32_t use_graph;     /* 1 = replay segments from a CUDA graph */
+    int32_t collect_stats; /* 1 = accumulate traffic counters (snp_result.stats) */
+} snp_run_opts;
+
+/* Host output rows for snp_advance.  Row i holds step (first_row_step + i):
+ * configs/delays are C_k/D_k (configs[k] of engine.py:143), spiking the
+ * chosen-rule ids of step k (-1 = none).  Any pointer may be NULL. */
+typedef struct snp_trace_out {
+    int64_t *configs;  /* [cap][q] */
+    int64_t *delays;   /* [cap][q] */
+    int64_t *spiking;  /* [cap][q] */
+    int64_t cap;       /* rows available */
+    int64_t first_row_step;  /* out: step of row 0 */
+    int64_t config_rows;     /* out: rows of configs/delays written */
+    int64_t spiking_rows;    /* out: rows of spiking written */
+} snp_trace_out;
+
+enum {
+    SNP_STAT_STEPS = 0,     /* steps executed with selection */
+    SNP_STAT_SCANNED,       /* sum over open neurons of rules scanned */
+    SNP_STAT_FIRED,         /* |F| */
+    SNP_STAT_SENDING,       /* fired with p > 0 */
+    SNP_STAT_EDGES,         /* adjacency entries read (gathered or pushed) */
+    SNP_STAT_ROWS,          /* reference walk rows: sum over sending of e + [e < z] */
+    SNP_STAT_OPEN,          /* open neurons (sum over steps) */
+    SNP_STAT_COUNT
+};
+
+typedef struct snp_result {
+    int64_t steps;         /* Trace.steps */
+    int32_t halt;          /* SNP_RUNNING / SNP_HALT_* */
+    int32_t error;         /* SNP_OK or SNP_ERR_NEGATIVE */
+    int64_t negative_neuron;  /* first neuron seen negative (error only) */
+    int64_t negative_value;
+    uint64_t stats[SNP_STAT_COUNT];
+    int64_t kernel_launches;  /* device kernels launched by this call */
+} snp_result;
+
+typedef struct snp_engine snp_engine;
+
+typedef struct snp_engine_info {
+    int64_t q, m, z;
+    int64_t device_bytes;     /* device memory held by the engine */
+    int32_t format, variant;
+    int32_t p_mode;           /* 0 bit (p common), 1 u8, 2 u16, 3 u32 */
+    int32_t heavy_neurons;
+    int64_t in_edges;         /* pull: padded in-adjacency entries */
+    int64_t p_common;
+} snp_engine_info;
+
+int snp_abi_version(void);
+const char *snp_last_error(void);
+int snp_device_count(void);
+
+int snp_engine_create(const snp_system_desc *desc, snp_engine **out);
+void snp_engine_destroy(snp_engine *eng);
+int snp_engine_get_info(const snp_engine *eng, snp_engine_info *info);
+
+/* Reset the run state to `initial` (host [q]; NULL = the system's own
+ * initial configuration) with every neuron open (engine.py:427-428). */
+int snp_begin(snp_engine *eng, const int64_t *initial);
+/* Execute up to `n_steps` more steps of the loop of engine.py:441-458,
+ * stopping early on halt / error or when `trace` (may be NULL) is full. */
+int snp_advance(snp_engine *eng, const snp_run_opts *opts, int64_t n_steps,
+                snp_trace_out *trace, snp_result *res);
+/* Final state after a halt: C and D (host int64 [q] each; either may be NULL). */
+int snp_read_state(snp_engine *eng, int64_t *config, int64_t *delays);
+/* snp_begin + snp_advance(to halt) + snp_read_state. */
+int snp_run(snp_engine *eng, const int64_t *initial, const snp_run_opts *opts,
+            int64_t *final_config, int64_t *final_delays, snp_result *res);
+/* Device-resident time of the last snp_advance/snp_run device loop (ms). */
+double snp_last_device_ms(const snp_engine *eng);
+
+/* Phase functions (engine.py:192-366), host arrays in, host arrays out. */
+int snp_sv_calc(snp_engine *eng, const int64_t *config, const int64_t *delays,
+                int32_t policy, uint64_t seed, int64_t step, int64_t *chosen);
+int snp_step(snp_engine *eng, const int64_t *config, const int64_t *delays,
+             const int64_t *chosen, int64_t *next_config, int64_t *row_visits);
+int snp_update_delays(snp_engine *eng, const int64_t *delays, const int64_t *chosen,
+                      int64_t *next_delays);
+
+/* Timing helper for benchmarks: run `steps` steps (no recording) from the
+ * current state with the device loop only and return the per-kernel mean
+ * duration of the dominant step kernel in *kernel_ms (CUDA events around
+ * each launch on the engine stream) and the total in *total_ms. */
+int snp_time_steps(snp_engine *eng, const snp_run_opts *opts, int64_t steps,
+                   double *total_ms, double *kernel_ms, snp_result *res);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SNPB200_H */

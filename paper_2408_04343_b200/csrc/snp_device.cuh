@@ -1,0 +1,792 @@
+// snp_device.cuh -- device layouts and sm_100a kernels of the SNP step engine.
+//
+// One simulation step of the reference (engine.py:441-458: sv_calc ->
+// step_{sparse,ell,compressed} -> update_delays -> halting test) is executed
+// as ONE fused, neuron-parallel kernel per step (`step_kernel`) plus, for the
+// push formats, the paper's scatter kernels:
+//
+//   step_kernel (k):   finish step k-1 for neuron j
+//                        C_k = Ĉ_{k-1} + [open_{k-1}(j)] * recv_{k-1}(j)
+//                        D_k = fired_{k-1} ? d : max(D_{k-1} - 1, 0)
+//                        (engine.py:263/307/352 + update_delays :358-366)
+//                      NegativeSpikes guard on C_k (engine.py:264)
+//                      select step k's rule (sv_calc, engine.py:192-236)
+//                        Ĉ_k = C_k - c[r]  (COMPRESSED consumes at selection)
+//                        publish P_k(j) = p[r] (pull) / chosen (push)
+//                      last CTA: halting decision (engine.py:443-450)
+//   push_kernel (k):   ELL (Alg. 4) / COMPRESSED-push (Alg. 5) scatter into
+//                      recv with 64-bit RED.ADD (engine.py:290-300, :338-345)
+//   dense_kernel (k):  S_k . M_Π over the fired rows (engine.py:257-262)
+//
+// recv(j) is either gathered from the in-adjacency (`pull`: sum of P_{k-1}
+// over in-neighbours, atomic-free) or read from the `recv` array written by
+// the push/dense kernels.  Deliveries to closed neurons are dropped at the
+// destination (the open gate above), which is exactly the reference's
+// per-target `delays[tgt] == 0` filter.
+//
+// All spike counts are int64 like the reference; thresholds / amounts /
+// delays are stored as int32 (range-checked at engine creation).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace snp {
+
+constexpr int kBlock = 256;
+constexpr uint32_t kLightRules = 32;   // thread-per-neuron selection (32-bit mask)
+constexpr uint32_t kLightIn = 256;     // thread-per-neuron gather
+constexpr uint32_t kLightOut = 64;     // thread-per-rule scatter
+constexpr uint32_t kExactBit = 0x80000000u;
+
+enum PMode { P_BIT = 0, P_U8 = 1, P_U16 = 2, P_U32 = 3 };
+enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
+enum Rec { REC_CONFIGS = 1, REC_DELAYS = 2, REC_SPIKING = 4 };
+enum Halt { RUNNING = 0, HALT_STEP_LIMIT = 1, HALT_NO_APPLICABLE = 2, HALT_NEGATIVE = 3 };
+enum Stat { ST_STEPS = 0, ST_SCANNED, ST_FIRED, ST_SENDING, ST_EDGES, ST_ROWS, ST_OPEN, ST_COUNT };
+
+// Run-control block in device memory.  Written by the last CTA of each
+// step kernel, read by every CTA of the next kernel; the host reads it after
+// each device loop segment.
+struct Ctrl {
+    long long step;          // k of the next step kernel
+    long long max_steps;     // SimOptions.max_steps
+    long long stop_at;       // segment end: kernels with step >= stop_at idle
+    long long trace_base;    // step of trace row 0
+    unsigned long long seed;
+    long long neg_index;
+    long long neg_value;
+    unsigned long long stats[8];
+    int policy;
+    int record;
+    int stats_on;
+    int halted;
+    int reason;
+    int fired_any;
+    int closed_any;
+    int neg_any;
+    unsigned int blocks_done;
+    int push_armed;          // a scatter for step (step-1) is pending
+    unsigned int list_count[2];   // dense fired-rule list, by step parity
+    unsigned int heavy_count[2];  // push heavy queue, by step parity
+};
+
+struct DevSys {
+    long long q;
+    long long m;
+    const uint32_t* roff;     // [q+1] rule offsets
+    const uint32_t* rthr;     // [m] threshold | exact << 31
+    const int4* rrec;         // [m] {consumed, produced, delay, outdeg(owner)}
+    const uint32_t* ioff;     // pull: [q+1] in-adjacency offsets (4-aligned)
+    const uint32_t* isrc;     // pull: sources, padded with the sentinel q
+    const uint32_t* soff;     // push COMPRESSED: [q+1] out-adjacency
+    const uint32_t* sdst;
+    const int2* ell;          // ELL: [m][ell_ld] (target, amount) pairs
+    const uint32_t* ell_len;  // ELL: live pairs per rule column
+    long long ell_ld;
+    const int* dense;         // SPARSE: [m][dense_ld]
+    long long dense_ld;
+    const uint32_t* heavy;    // CTA-per-neuron list
+    int n_heavy;
+    int light_blocks;
+    int z;                    // max out-degree
+    int ell_rows;             // z + 1
+    long long p_common;       // P_BIT: the single produced amount
+};
+
+struct DevState {
+    long long* cfg;           // Ĉ (C after this step's consumption)
+    int* ds;                  // delay state, see decode_ds
+    int* chosen;              // [q] chosen rule (push/dense formats, phase API)
+    uint32_t* P[3];           // pull exchange vectors (triple buffered)
+    long long* recv;          // push/dense accumulation
+    uint32_t* list[2];        // fired rules (dense) / heavy queue (push), by parity
+    Ctrl* ctrl;
+    long long* tr_cfg;        // [tr_rows][q]
+    int* tr_dly;
+    int* tr_chosen;
+    long long tr_rows;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+
+// Kernel-parameter arrays indexed with a runtime value are spilled to the
+// stack; select through branches instead.
+__device__ __forceinline__ uint32_t* pick3(uint32_t* const (&a)[3], long long i) {
+    return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
+}
+__device__ __forceinline__ uint32_t* pick2(uint32_t* const (&a)[2], long long i) {
+    return (i & 1) ? a[1] : a[0];
+}
+
+// selection.py:37-45 -- SplitMix64-style finaliser, wrapping uint64.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long seed, long long step,
+                                                    long long neuron) {
+    unsigned long long z = seed + 0x9E3779B97F4A7C15ull * (unsigned long long)(step + 1) +
+                           0xBF58476D1CE4E5B9ull * (unsigned long long)(neuron + 1);
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+// Delay state word: ds < 0  -> fired last step with delay d = -ds-1 (open then)
+//                   ds >= 0 -> did not fire; ds is that step's delay counter.
+__device__ __forceinline__ bool ds_open(int ds) { return ds <= 0; }
+__device__ __forceinline__ int ds_next(int ds) { return ds < 0 ? -ds - 1 : (ds > 0 ? ds - 1 : 0); }
+
+// regex guard (model.py:58-61)
+__device__ __forceinline__ bool guard_ok(uint32_t w, long long count) {
+    long long t = (long long)(w & ~kExactBit);
+    return (w & kExactBit) ? count == t : count >= t;
+}
+
+// position of the (k+1)-th set bit of mask (k < popc(mask))
+__device__ __forceinline__ int nth_set_bit(uint32_t mask, uint32_t k) {
+#pragma unroll 1
+    for (uint32_t i = 0; i < k; ++i) mask &= mask - 1;
+    return __ffs(mask) - 1;
+}
+
+__device__ __forceinline__ void red_add_i64(long long* addr, long long v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(v));
+}
+
+template <int PM>
+__device__ __forceinline__ long long p_lookup(const uint32_t* __restrict__ P, uint32_t s) {
+    if constexpr (PM == P_BIT) {
+        return (__ldg(P + (s >> 5)) >> (s & 31)) & 1u;
+    } else if constexpr (PM == P_U8) {
+        return __ldg(reinterpret_cast<const uint8_t*>(P) + s);
+    } else if constexpr (PM == P_U16) {
+        return __ldg(reinterpret_cast<const uint16_t*>(P) + s);
+    } else {
+        return __ldg(P + s);
+    }
+}
+
+// Thread-serial gather over a 4-aligned, sentinel-padded in-list.
+template <int PM>
+__device__ __forceinline__ long long gather_thread(const uint32_t* __restrict__ isrc,
+                                                   const uint32_t* __restrict__ P,
+                                                   uint32_t e0, uint32_t e1) {
+    long long acc = 0;
+    const uint4* p4 = reinterpret_cast<const uint4*>(isrc + e0);
+    const uint32_t n4 = (e1 - e0) >> 2;
+#pragma unroll 4
+    for (uint32_t i = 0; i < n4; ++i) {
+        uint4 v = __ldg(p4 + i);
+        acc += p_lookup<PM>(P, v.x) + p_lookup<PM>(P, v.y) + p_lookup<PM>(P, v.z) +
+               p_lookup<PM>(P, v.w);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+struct BlockStats {
+    unsigned long long v[ST_COUNT];
+};
+
+// Block-wide reduction of per-thread stats into Ctrl (one atomic per counter).
+__device__ __forceinline__ void flush_stats(Ctrl* ctl, unsigned long long (&loc)[ST_COUNT]) {
+    __shared__ unsigned long long sh[ST_COUNT];
+    if (threadIdx.x < ST_COUNT) sh[threadIdx.x] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ST_COUNT; ++i) {
+        unsigned long long v = loc[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sh[i], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < ST_COUNT && sh[threadIdx.x]) atomicAdd(&ctl->stats[threadIdx.x], sh[threadIdx.x]);
+}
+
+// Last-CTA-done: halting decision for step k (engine.py:443-450) and reset
+// of the per-step flags.  Called by thread 0 of every CTA.
+__device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bool bf, bool bc,
+                                            bool bn, long long neg_idx, long long neg_val) {
+    if (bf) atomicOr(&ctl->fired_any, 1);
+    if (bc) atomicOr(&ctl->closed_any, 1);
+    if (bn) {
+        atomicOr(&ctl->neg_any, 1);
+        long long prev = atomicMin(&ctl->neg_index, neg_idx);
+        if (neg_idx < prev) ctl->neg_value = neg_val;  // best effort (diagnostics only)
+    }
+    __threadfence();
+    unsigned int done = atomicAdd(&ctl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    __threadfence();
+    volatile Ctrl* v = ctl;
+    const int fired = v->fired_any, closed = v->closed_any, neg = v->neg_any;
+    v->fired_any = 0;
+    v->closed_any = 0;
+    v->blocks_done = 0;
+    // counters used by the NEXT step (parity (k+1)&1) start from zero
+    v->list_count[(k + 1) & 1] = 0;
+    v->heavy_count[(k + 1) & 1] = 0;
+    int armed = 0;
+    if (neg) {
+        v->halted = 1;
+        v->reason = HALT_NEGATIVE;
+    } else if (!sel) {
+        v->halted = 1;
+        v->reason = HALT_STEP_LIMIT;
+    } else if (!fired && !closed) {
+        v->halted = 1;
+        v->reason = HALT_NO_APPLICABLE;
+    } else {
+        v->step = k + 1;
+        armed = 1;
+        if (v->stats_on) v->stats[ST_STEPS] += 1;
+    }
+    v->push_armed = armed;
+    __threadfence();
+}
+
+// ---------------------------------------------------------------------------
+// The fused step kernel.
+//
+// CTAs [0, light_blocks) map thread -> neuron j = blockIdx*256 + tid (light
+// neurons: <= 32 rules and, for pull, in-degree <= 256).  CTAs beyond that
+// each own one heavy neuron from s.heavy (e.g. the sorter's detectors with n
+// rules and n in-neighbours): block-strided gather + block-wide ballot scan.
+
+template <int KIND, int PM, bool CONSUME, bool FLIST>
+__global__ void __launch_bounds__(kBlock) step_kernel(DevSys s, DevState st) {
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    const int halted = vc->halted;
+    const long long k = vc->step;
+    if (halted || k >= vc->stop_at) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->push_armed = 0;
+        return;
+    }
+    const bool sel = k < vc->max_steps;
+    const int policy = vc->policy;
+    const unsigned long long seed = vc->seed;
+    const int record = vc->record;
+    const bool stats_on = vc->stats_on != 0;
+    const long long slot = k - vc->trace_base;
+    const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
+    uint32_t* Pcur = pick3(st.P, k % 3);
+    uint32_t* Pzero = pick3(st.P, (k + 1) % 3);
+    const bool want_chosen = (KIND == RECV_ARRAY);
+    const long long q = s.q;
+
+    unsigned long long stat[ST_COUNT];
+#pragma unroll
+    for (int i = 0; i < ST_COUNT; ++i) stat[i] = 0;
+    bool t_fired = false, t_closed = false, t_neg = false;
+    long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
+
+    if (blockIdx.x < (unsigned)s.light_blocks) {
+        // ------------------------------------------------------------ light
+        const long long j = (long long)blockIdx.x * kBlock + threadIdx.x;
+        const bool active = j < q;
+        uint32_t r0 = 0, r1 = 0, e0 = 0, e1 = 0;
+        if (active) {
+            r0 = __ldg(s.roff + j);
+            r1 = __ldg(s.roff + j + 1);
+            if (KIND == RECV_PULL) {
+                e0 = __ldg(s.ioff + j);
+                e1 = __ldg(s.ioff + j + 1);
+            }
+        }
+        const bool heavy = active && ((r1 - r0) > kLightRules ||
+                                      (KIND == RECV_PULL && (e1 - e0) > kLightIn));
+        const bool mine = active && !heavy;
+        int r = -1;
+        long long pval = 0;
+        if (mine) {
+            long long C = st.cfg[j];
+            const int dsv = st.ds[j];
+            const bool open_prev = ds_open(dsv);
+            if (KIND == RECV_PULL) {
+                if (open_prev && e1 > e0) {
+                    long long g = gather_thread<PM>(s.isrc, Pprev, e0, e1);
+                    C += (PM == P_BIT) ? g * s.p_common : g;
+                    stat[ST_EDGES] += e1 - e0;
+                }
+            } else {
+                const long long rv = st.recv[j];
+                if (rv != 0) st.recv[j] = 0;
+                if (open_prev) C += rv;
+            }
+            const int D = ds_next(dsv);
+            if (C < 0) {
+                t_neg = true;
+                neg_idx = j;
+                neg_val = C;
+            }
+            if (record & REC_CONFIGS) st.tr_cfg[slot * q + j] = C;
+            if (record & REC_DELAYS) st.tr_dly[slot * q + j] = D;
+            t_closed = D != 0;
+            if (sel && D == 0) {
+                const uint32_t nr = r1 - r0;
+                uint32_t mask = 0;
+                for (uint32_t t = 0; t < nr; ++t) mask |= (uint32_t)guard_ok(__ldg(s.rthr + r0 + t), C) << t;
+                stat[ST_OPEN] += 1;
+                if (mask) {
+                    int idx;
+                    if (policy == 0) {
+                        idx = __ffs(mask) - 1;
+                        stat[ST_SCANNED] += idx + 1;
+                    } else {
+                        const uint32_t cnt = __popc(mask);
+                        idx = nth_set_bit(mask, (uint32_t)(mix64(seed, k, j) % cnt));
+                        stat[ST_SCANNED] += nr;
+                    }
+                    r = (int)(r0 + idx);
+                } else {
+                    stat[ST_SCANNED] += nr;
+                }
+            }
+            int nds = D;
+            long long Cn = C;
+            if (r >= 0) {
+                const int4 rec = __ldg(s.rrec + r);
+                if (CONSUME) Cn -= rec.x;
+                pval = rec.y;
+                nds = -(rec.z + 1);
+                t_fired = true;
+                stat[ST_FIRED] += 1;
+                if (pval > 0) {
+                    stat[ST_SENDING] += 1;
+                    stat[ST_ROWS] += (unsigned long long)rec.w + (rec.w < s.z ? 1 : 0);
+                }
+                if (FLIST) {
+                    unsigned int pos = atomicAdd(&ctl->list_count[k & 1], 1u);
+                    pick2(st.list, k)[pos] = (uint32_t)r;
+                }
+            }
+            st.cfg[j] = Cn;
+            st.ds[j] = nds;
+            if (sel) {
+                if (want_chosen) st.chosen[j] = r;
+                if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
+                if (KIND == RECV_PULL && PM != P_BIT) {
+                    if (PM == P_U8) reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)pval;
+                    else if (PM == P_U16) reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)pval;
+                    else Pcur[j] = (uint32_t)pval;
+                }
+            }
+        }
+        if (KIND == RECV_PULL && PM == P_BIT && sel) {
+            // one 32-neuron word per warp: lanes are consecutive neurons
+            const unsigned int bits = __ballot_sync(0xffffffffu, mine && pval > 0);
+            const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
+            const unsigned int act = __ballot_sync(0xffffffffu, active);
+            if ((threadIdx.x & 31) == 0 && act) {
+                const long long w = j >> 5;
+                Pzero[w] = 0u;
+                if (hv) {
+                    if (bits) atomicOr(Pcur + w, bits);
+                } else {
+                    Pcur[w] = bits;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ heavy
+        __shared__ long long sh_sum[kBlock / 32];
+        __shared__ int sh_pick;
+        __shared__ unsigned int sh_cnt[kBlock / 32];
+        const int h = blockIdx.x - s.light_blocks;
+        const long long j = s.heavy[h];
+        const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
+        long long C = st.cfg[j];
+        const int dsv = st.ds[j];
+        const bool open_prev = ds_open(dsv);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (KIND == RECV_PULL) {
+            long long part = 0;
+            if (open_prev) {
+                const uint32_t e0 = __ldg(s.ioff + j), e1 = __ldg(s.ioff + j + 1);
+                for (uint32_t e = e0 + threadIdx.x; e < e1; e += kBlock) part += p_lookup<PM>(Pprev, __ldg(s.isrc + e));
+                if (threadIdx.x == 0) stat[ST_EDGES] += e1 - e0;
+            }
+            part = warp_sum_ll(part);
+            if (lane == 0) sh_sum[wid] = part;
+            __syncthreads();
+            long long g = 0;
+#pragma unroll
+            for (int w = 0; w < kBlock / 32; ++w) g += sh_sum[w];
+            C += (PM == P_BIT) ? g * s.p_common : g;
+        } else {
+            const long long rv = st.recv[j];
+            __syncthreads();
+            if (threadIdx.x == 0 && rv != 0) st.recv[j] = 0;
+            if (open_prev) C += rv;
+        }
+        const int D = ds_next(dsv);
+        if (threadIdx.x == 0) {
+            if (C < 0) {
+                t_neg = true;
+                neg_idx = j;
+                neg_val = C;
+            }
+            if (record & REC_CONFIGS) st.tr_cfg[slot * q + j] = C;
+            if (record & REC_DELAYS) st.tr_dly[slot * q + j] = D;
+            t_closed = D != 0;
+        }
+        int r = -1;
+        if (sel && D == 0) {
+            if (threadIdx.x == 0) {
+                sh_pick = -1;
+                stat[ST_OPEN] += 1;
+            }
+            __syncthreads();
+            if (policy == 0) {
+                for (uint32_t base = r0; base < r1; base += kBlock) {
+                    const uint32_t t = base + threadIdx.x;
+                    const bool ok = t < r1 && guard_ok(__ldg(s.rthr + t), C);
+                    if (__syncthreads_or(ok)) {
+                        const unsigned int b = __ballot_sync(0xffffffffu, ok);
+                        if (lane == 0 && b) atomicMin(reinterpret_cast<unsigned int*>(&sh_pick),
+                                                      base + wid * 32 + __ffs(b) - 1);
+                        __syncthreads();
+                        break;
+                    }
+                }
+                // sh_pick initialised to -1 == 0xffffffff (unsigned max)
+                r = sh_pick;
+                if (threadIdx.x == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
+            } else {
+                uint32_t total = 0;
+                for (uint32_t base = r0; base < r1; base += kBlock) {
+                    const uint32_t t = base + threadIdx.x;
+                    total += __syncthreads_count(t < r1 && guard_ok(__ldg(s.rthr + t), C));
+                }
+                if (threadIdx.x == 0) stat[ST_SCANNED] += r1 - r0;
+                if (total) {
+                    uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
+                    for (uint32_t base = r0; base < r1; base += kBlock) {
+                        const uint32_t t = base + threadIdx.x;
+                        const bool ok = t < r1 && guard_ok(__ldg(s.rthr + t), C);
+                        const uint32_t c = __syncthreads_count(ok);
+                        if (want < c) {
+                            const unsigned int b = __ballot_sync(0xffffffffu, ok);
+                            if (lane == 0) sh_cnt[wid] = __popc(b);
+                            __syncthreads();
+                            uint32_t before = 0;
+                            for (int w = 0; w < wid; ++w) before += sh_cnt[w];
+                            const uint32_t rank = before + __popc(b & ((1u << lane) - 1u));
+                            if (ok && rank == want) sh_pick = (int)t;
+                            __syncthreads();
+                            break;
+                        }
+                        want -= c;
+                    }
+                    r = sh_pick;
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            int nds = D;
+            long long Cn = C;
+            long long pval = 0;
+            if (r >= 0) {
+                const int4 rec = __ldg(s.rrec + r);
+                if (CONSUME) Cn -= rec.x;
+                pval = rec.y;
+                nds = -(rec.z + 1);
+                t_fired = true;
+                stat[ST_FIRED] += 1;
+                if (pval > 0) {
+                    stat[ST_SENDING] += 1;
+                    stat[ST_ROWS] += (unsigned long long)rec.w + (rec.w < s.z ? 1 : 0);
+                }
+                if (FLIST) {
+                    unsigned int pos = atomicAdd(&ctl->list_count[k & 1], 1u);
+                    pick2(st.list, k)[pos] = (uint32_t)r;
+                }
+            }
+            st.cfg[j] = Cn;
+            st.ds[j] = nds;
+            if (sel) {
+                if (want_chosen) st.chosen[j] = r;
+                if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
+                if (KIND == RECV_PULL) {
+                    if (PM == P_BIT) {
+                        if (pval > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
+                    } else if (PM == P_U8) {
+                        reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)pval;
+                    } else if (PM == P_U16) {
+                        reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)pval;
+                    } else {
+                        Pcur[j] = (uint32_t)pval;
+                    }
+                }
+            }
+        }
+    }
+
+    if (stats_on) flush_stats(ctl, stat);
+    const bool bf = __syncthreads_or(t_fired);
+    const bool bc = __syncthreads_or(t_closed);
+    // negative: smallest index within the block
+    __shared__ long long sh_neg_idx, sh_neg_val;
+    if (threadIdx.x == 0) sh_neg_idx = 0x7fffffffffffffffll;
+    __syncthreads();
+    if (t_neg) atomicMin(&sh_neg_idx, neg_idx);
+    __syncthreads();
+    if (t_neg && sh_neg_idx == neg_idx) sh_neg_val = neg_val;
+    const bool bn = __syncthreads_or(t_neg);
+    if (threadIdx.x == 0) finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Push scatter (paper Alg. 4 ELL / Alg. 5 Optimized) for step k = step-1.
+// Thread per neuron; columns longer than kLightOut go to the heavy queue.
+
+template <bool ELL>
+__global__ void __launch_bounds__(kBlock) push_kernel(DevSys s, DevState st, long long* row_visits) {
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    if (!vc->push_armed) return;
+    const long long k = vc->step - 1;
+    const bool stats_on = vc->stats_on != 0;
+    unsigned long long edges = 0;
+    const long long j = (long long)blockIdx.x * kBlock + threadIdx.x;
+    if (j < s.q) {
+        const int r = st.chosen[j];
+        if (r >= 0) {
+            if (ELL) {
+                const uint32_t len = __ldg(s.ell_len + r);
+                if (row_visits) row_visits[r] += len + (len < (uint32_t)s.ell_rows ? 1 : 0);
+                if (len <= kLightOut) {
+                    const int2* col = s.ell + (long long)r * s.ell_ld;
+                    for (uint32_t i = 0; i < len; ++i) {
+                        const int2 pr = __ldg(col + i);
+                        red_add_i64(st.recv + pr.x, pr.y);
+                    }
+                    edges += len;
+                } else {
+                    unsigned int pos = atomicAdd(&ctl->heavy_count[k & 1], 1u);
+                    pick2(st.list, k)[pos] = (uint32_t)j;
+                }
+            } else {
+                const int p = __ldg(s.rrec + r).y;
+                if (p > 0) {
+                    const uint32_t e0 = __ldg(s.soff + j), e1 = __ldg(s.soff + j + 1);
+                    if (e1 - e0 <= kLightOut) {
+                        for (uint32_t e = e0; e < e1; ++e) red_add_i64(st.recv + __ldg(s.sdst + e), p);
+                        edges += e1 - e0;
+                    } else {
+                        unsigned int pos = atomicAdd(&ctl->heavy_count[k & 1], 1u);
+                        pick2(st.list, k)[pos] = (uint32_t)j;
+                    }
+                }
+            }
+        }
+    }
+    if (stats_on) {
+        edges = warp_sum_ll((long long)edges);
+        if ((threadIdx.x & 31) == 0 && edges) atomicAdd(&ctl->stats[ST_EDGES], edges);
+    }
+}
+
+// Warp per queued heavy column.
+template <bool ELL>
+__global__ void __launch_bounds__(kBlock) push_heavy_kernel(DevSys s, DevState st) {
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    if (!vc->push_armed) return;
+    const long long k = vc->step - 1;
+    const unsigned int n = vc->heavy_count[k & 1];
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (kBlock / 32);
+    unsigned long long edges = 0;
+    for (long long w = (long long)blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); w < n; w += warps) {
+        const uint32_t j = pick2(st.list, k)[w];
+        const int r = st.chosen[j];
+        if (ELL) {
+            const uint32_t len = __ldg(s.ell_len + r);
+            const int2* col = s.ell + (long long)r * s.ell_ld;
+            for (uint32_t i = lane; i < len; i += 32) {
+                const int2 pr = __ldg(col + i);
+                red_add_i64(st.recv + pr.x, pr.y);
+            }
+            edges += len;
+        } else {
+            const int p = __ldg(s.rrec + r).y;
+            const uint32_t e0 = __ldg(s.soff + j), e1 = __ldg(s.soff + j + 1);
+            for (uint32_t e = e0 + lane; e < e1; e += 32) red_add_i64(st.recv + __ldg(s.sdst + e), p);
+            edges += e1 - e0;
+        }
+    }
+    if (vc->stats_on && lane == 0 && edges) atomicAdd(&ctl->stats[ST_EDGES], edges);
+}
+
+// Dense S.M (paper Alg. 3 over the fired rows only): blockIdx.x tiles 1024
+// columns (int4 per thread), blockIdx.y splits the fired-rule list.
+__global__ void __launch_bounds__(kBlock) dense_kernel(DevSys s, DevState st) {
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    if (!vc->push_armed) return;
+    const long long k = vc->step - 1;
+    const unsigned int n = vc->list_count[k & 1];
+    const long long c4 = ((long long)blockIdx.x * kBlock + threadIdx.x) * 4;
+    if (c4 >= s.q) return;
+    const unsigned int lo = (unsigned int)((unsigned long long)n * blockIdx.y / gridDim.y);
+    const unsigned int hi = (unsigned int)((unsigned long long)n * (blockIdx.y + 1) / gridDim.y);
+    long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    const uint32_t* lst = pick2(st.list, k);
+    for (unsigned int f = lo; f < hi; ++f) {
+        const uint32_t r = lst[f];
+        const int4 v = __ldg(reinterpret_cast<const int4*>(s.dense + (long long)r * s.dense_ld + c4));
+        a0 += v.x;
+        a1 += v.y;
+        a2 += v.z;
+        a3 += v.w;
+    }
+    if (a0) red_add_i64(st.recv + c4, a0);
+    if (a1 && c4 + 1 < s.q) red_add_i64(st.recv + c4 + 1, a1);
+    if (a2 && c4 + 2 < s.q) red_add_i64(st.recv + c4 + 2, a2);
+    if (a3 && c4 + 3 < s.q) red_add_i64(st.recv + c4 + 3, a3);
+    if (vc->stats_on && blockIdx.x == 0 && threadIdx.x == 0 && blockIdx.y == 0)
+        atomicAdd(&ctl->stats[ST_EDGES], (unsigned long long)n * (unsigned long long)s.q);
+}
+
+// ---------------------------------------------------------------------------
+// Phase-API helpers.
+
+// Load an arbitrary (C, D, chosen) as the engine state right after the
+// selection of step 0 (engine.py:239-355 take the spiking vector as input).
+// The source-open re-check of engine.py:252/281/321 applies: a chosen rule
+// of a closed neuron is ignored.
+template <int KIND, int PM, bool CONSUME, bool FLIST>
+__global__ void prime_kernel(DevSys s, DevState st, const long long* __restrict__ C,
+                             const long long* __restrict__ D, const long long* __restrict__ chosen) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= s.q) return;
+    long long r = chosen[j];
+    const long long d = D[j];
+    if (d != 0) r = -1;
+    long long c = C[j];
+    int nds = (int)d;
+    long long pval = 0;
+    if (r >= 0) {
+        const int4 rec = s.rrec[r];
+        if (CONSUME) c -= rec.x;
+        pval = rec.y;
+        nds = -(rec.z + 1);
+        if (FLIST) {
+            unsigned int pos = atomicAdd(&st.ctrl->list_count[0], 1u);
+            st.list[0][pos] = (uint32_t)r;
+        }
+    }
+    st.cfg[j] = c;
+    st.ds[j] = nds;
+    if (KIND == RECV_ARRAY) {
+        st.chosen[j] = (int)r;
+    } else if (PM == P_BIT) {
+        if (pval > 0) atomicOr(st.P[0] + (j >> 5), 1u << (j & 31));
+    } else if (PM == P_U8) {
+        reinterpret_cast<uint8_t*>(st.P[0])[j] = (uint8_t)pval;
+    } else if (PM == P_U16) {
+        reinterpret_cast<uint16_t*>(st.P[0])[j] = (uint16_t)pval;
+    } else {
+        st.P[0][j] = (uint32_t)pval;
+    }
+}
+
+// update_delays (engine.py:358-366): no source-open filter, like the reference.
+__global__ void update_delays_kernel(long long q, const int4* __restrict__ rrec,
+                                     const long long* __restrict__ D,
+                                     const long long* __restrict__ chosen, long long* out) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= q) return;
+    const long long r = chosen[j];
+    const long long d = D[j];
+    out[j] = r >= 0 ? (long long)rrec[r].z : (d > 0 ? d - 1 : 0);
+}
+
+// Load (C, D) so that the next step kernel finalises exactly C_k = C, D_k = D
+// and then selects (sv_calc of engine.py:192-236).
+__global__ void load_state_kernel(long long q, long long* cfg, int* ds, const long long* __restrict__ C,
+                                  const long long* __restrict__ D) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= q) return;
+    cfg[j] = C[j];
+    ds[j] = (int)(D[j] + 1);  // ds_next(D+1) == D, and not "open last step"
+}
+
+__global__ void widen_i32_kernel(long long n, const int* __restrict__ in, long long* out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[i];
+}
+
+// D_k from the delay state after a halt (the last kernel ran without selection).
+__global__ void ds_to_delay_kernel(long long q, const int* __restrict__ ds, long long* out) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < q) {
+        const int v = ds[j];
+        out[j] = v < 0 ? -v - 1 : v;  // after a halt ds holds D_k directly (no firing)
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Device-side layout builders (from the CSR out-adjacency).
+
+// In-degree histogram of the transpose.
+__global__ void indeg_kernel(long long S, const uint32_t* __restrict__ dst, uint32_t* indeg) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < S;
+         e += (long long)gridDim.x * blockDim.x)
+        atomicAdd(indeg + dst[e], 1u);
+}
+
+// Scatter sources into their destination lists (cursor = padded offsets).
+__global__ void transpose_fill_kernel(long long q, const uint32_t* __restrict__ soff,
+                                      const uint32_t* __restrict__ sdst, uint32_t* cursor,
+                                      uint32_t* isrc) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= q) return;
+    for (uint32_t e = soff[i]; e < soff[i + 1]; ++e) {
+        const uint32_t pos = atomicAdd(cursor + sdst[e], 1u);
+        isrc[pos] = (uint32_t)i;
+    }
+}
+
+// ELL columns per rule: (owner, -c) then (dst, p) for sending rules.
+__global__ void build_ell_kernel(long long m, long long ld, const uint32_t* __restrict__ owner,
+                                 const int4* __restrict__ rrec, const uint32_t* __restrict__ soff,
+                                 const uint32_t* __restrict__ sdst, int2* ell, uint32_t* len) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint32_t o = owner[r];
+    const int4 rec = rrec[r];
+    int2* col = ell + r * ld;
+    col[0] = make_int2((int)o, -rec.x);
+    uint32_t n = 1;
+    if (rec.y > 0) {
+        for (uint32_t e = soff[o]; e < soff[o + 1]; ++e) col[n++] = make_int2((int)sdst[e], rec.y);
+    }
+    len[r] = n;
+}
+
+// Dense rows: -c at the owner, +p at every out-neighbour (matrices.py:143-154).
+__global__ void build_dense_kernel(long long m, long long ld, const uint32_t* __restrict__ owner,
+                                   const int4* __restrict__ rrec, const uint32_t* __restrict__ soff,
+                                   const uint32_t* __restrict__ sdst, int* dense) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint32_t o = owner[r];
+    const int4 rec = rrec[r];
+    int* row = dense + r * ld;
+    row[o] = -rec.x;
+    if (rec.y > 0)
+        for (uint32_t e = soff[o]; e < soff[o + 1]; ++e) row[sdst[e]] = rec.y;
+}
+
+}  // namespace snp

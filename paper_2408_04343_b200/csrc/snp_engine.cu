@@ -1,0 +1,946 @@
+// snp_engine.cu -- host runtime + C ABI (include/snpb200.h) of the B200 SNP
+// step engine.  Owns all device memory of an engine; builds the device
+// layouts from the reference's interchange arrays (RuleVector,
+// NeuronRuleMap, and either a CSR out-adjacency or the format's own matrix);
+// drives the per-step kernels of snp_device.cuh as CUDA-graph segments with
+// device-side halting; and implements the phase-level entry points.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/snpb200.h"
+#include "snp_device.cuh"
+
+using namespace snp;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CU(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            return fail(e_ == cudaErrorMemoryAllocation ? SNP_ERR_CAPACITY : SNP_ERR_CUDA,        \
+                        "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__,          \
+                        __LINE__);                                                                \
+        }                                                                                         \
+    } while (0)
+
+#define TRY(expr)                \
+    do {                         \
+        int rc_ = (expr);        \
+        if (rc_ != SNP_OK) return rc_; \
+    } while (0)
+
+constexpr long long kInt32Max = 2147483647ll;
+
+inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+using StepFn = void (*)(DevSys, DevState);
+using PrimeFn = void (*)(DevSys, DevState, const long long*, const long long*, const long long*);
+
+template <int KIND, int PM, bool CONSUME, bool FLIST>
+void pick_fns(StepFn* step, PrimeFn* prime) {
+    *step = step_kernel<KIND, PM, CONSUME, FLIST>;
+    *prime = prime_kernel<KIND, PM, CONSUME, FLIST>;
+}
+
+}  // namespace
+
+struct snp_engine {
+    int format = SNP_FMT_COMPRESSED;
+    int variant = SNP_VARIANT_PULL;
+    int device = 0;
+    long long q = 0, m = 0;
+    int z = 0;
+    int p_mode = P_BIT;
+    long long p_common = 1;
+    long long in_edges = 0;
+    int kind = RECV_PULL;
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    long long device_bytes = 0;
+    std::vector<long long> initial;  // host copy of the system's C_0
+    DevSys sys{};
+    DevState st{};
+    StepFn step_fn = nullptr;
+    PrimeFn prime_fn = nullptr;
+    int step_grid = 0;
+    int push_grid = 0;
+    int heavy_push_grid = 0;
+    dim3 dense_grid;
+    // run state
+    Ctrl hctrl{};
+    bool begun = false;
+    // graph cache
+    cudaGraphExec_t graph = nullptr;
+    long long graph_iters = 0;
+    long long tr_rows = 0;
+    // phase scratch
+    long long* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_ms = 0.0;
+
+    template <typename T>
+    int alloc(T** p, long long count) {
+        size_t bytes = (size_t)std::max<long long>(count, 1) * sizeof(T);
+        void* ptr = nullptr;
+        cudaError_t e = cudaMalloc(&ptr, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SNP_ERR_CAPACITY, "cudaMalloc of %zu bytes failed: %s", bytes,
+                        cudaGetErrorString(e));
+        }
+        allocs.push_back(ptr);
+        device_bytes += (long long)bytes;
+        *p = static_cast<T*>(ptr);
+        return SNP_OK;
+    }
+
+    ~snp_engine() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (void* p : allocs) cudaFree(p);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+template <typename T>
+int upload(snp_engine* e, T** dptr, const std::vector<T>& host) {
+    TRY(e->alloc(dptr, (long long)host.size()));
+    if (!host.empty()) CU(cudaMemcpy(*dptr, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return SNP_OK;
+}
+
+__global__ void fill_u32_kernel(long long n, uint32_t* p, uint32_t v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+int grid_for(long long n, int block = 256) {
+    return (int)std::max<long long>(1, std::min<long long>(ceil_div(n, block), 1ll << 30));
+}
+
+// Build every device structure.  Host-side work is O(q + m + S) with plain
+// loops; the quadratic layouts (ELL pairs, dense rows) and the in-adjacency
+// transpose are built on the device.
+int build(snp_engine* e, const snp_system_desc* d) {
+    const long long q = d->q, m = d->m;
+    if (q < 0 || m < 0) return fail(SNP_ERR_BAD_ARG, "q and m must be >= 0");
+    if (q >= kInt32Max) return fail(SNP_ERR_CAPACITY, "q=%lld exceeds the int32 neuron index range", q);
+    if (m >= (1ll << 32) - 1) return fail(SNP_ERR_CAPACITY, "m=%lld exceeds the uint32 rule index range", m);
+    if (q > 0 && (!d->initial || !d->offsets)) return fail(SNP_ERR_BAD_ARG, "initial/offsets missing");
+    if (m > 0 && (!d->threshold || !d->is_exact || !d->consumed || !d->produced || !d->delay))
+        return fail(SNP_ERR_BAD_ARG, "rule vector arrays missing");
+    e->q = q;
+    e->m = m;
+    e->format = d->format;
+    e->initial.assign(d->initial, d->initial + q);
+    for (long long i = 0; i < q; ++i)
+        if (d->initial[i] < 0) return fail(SNP_ERR_BAD_ARG, "initial spike count of neuron %lld is negative", i);
+
+    // --- rule vector + offsets (matrices.py:48-73, 115-140)
+    if (q > 0 && d->offsets[0] != 0) return fail(SNP_ERR_BAD_ARG, "offsets[0] must be 0");
+    std::vector<uint32_t> roff(q + 1, 0), owner(m);
+    for (long long i = 0; i < q; ++i) {
+        const long long a = d->offsets[i], b = d->offsets[i + 1];
+        if (b < a || b > m) return fail(SNP_ERR_BAD_ARG, "offsets not non-decreasing within [0, m]");
+        roff[i + 1] = (uint32_t)b;
+        for (long long r = a; r < b; ++r) owner[r] = (uint32_t)i;
+    }
+    if ((q > 0 ? d->offsets[q] : 0) != m) return fail(SNP_ERR_BAD_ARG, "offsets[q] != m");
+    std::vector<uint32_t> rthr(m);
+    std::vector<int4> rrec(m);
+    long long pmax = 0, pfirst = -1;
+    bool pcommon = true;
+    for (long long r = 0; r < m; ++r) {
+        const long long t = d->threshold[r], c = d->consumed[r], p = d->produced[r], dl = d->delay[r];
+        if (t < 0 || t > kInt32Max) return fail(SNP_ERR_CAPACITY, "rule %lld threshold %lld outside [0, 2^31-1]", r, t);
+        if (c < 0 || c > kInt32Max || p < 0 || p > kInt32Max)
+            return fail(SNP_ERR_CAPACITY, "rule %lld consumed/produced outside [0, 2^31-1]", r);
+        if (dl < 0 || dl > kInt32Max - 2) return fail(SNP_ERR_CAPACITY, "rule %lld delay %lld outside [0, 2^31-3]", r, dl);
+        rthr[r] = (uint32_t)t | (d->is_exact[r] ? kExactBit : 0u);
+        rrec[r] = make_int4((int)c, (int)p, (int)dl, 0);
+        if (p > 0) {
+            pmax = std::max(pmax, p);
+            if (pfirst < 0) pfirst = p;
+            else if (p != pfirst) pcommon = false;
+        }
+    }
+
+    // --- transition structure
+    std::vector<uint32_t> soff, sdst;
+    bool have_adj = false;
+    if (d->adj_offsets) {
+        soff.resize(q + 1);
+        const long long S = q > 0 ? d->adj_offsets[q] : 0;
+        if (S >= (1ll << 32) - 1) return fail(SNP_ERR_CAPACITY, "synapse count %lld exceeds uint32", S);
+        sdst.resize(S);
+        for (long long i = 0; i <= q; ++i) soff[i] = (uint32_t)d->adj_offsets[i];
+        for (long long s = 0; s < S; ++s) {
+            const long long t = d->adj_targets[s];
+            if (t < 0 || t >= q) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", t);
+            sdst[s] = (uint32_t)t;
+        }
+        have_adj = true;
+    } else if (d->syn_target && e->format == SNP_FMT_COMPRESSED) {
+        // SynapseMatrix [rows][q]: the first NULL ends a column (matrices.py:100-112)
+        soff.assign(q + 1, 0);
+        for (long long i = 0; i < q; ++i) {
+            long long n = 0;
+            while (n < d->syn_rows && d->syn_target[n * q + i] >= 0) ++n;
+            soff[i + 1] = soff[i] + (uint32_t)n;
+        }
+        sdst.resize(soff[q]);
+        for (long long i = 0; i < q; ++i)
+            for (uint32_t n = 0; n < soff[i + 1] - soff[i]; ++n) {
+                const long long t = d->syn_target[(long long)n * q + i];
+                if (t >= q) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", t);
+                sdst[soff[i] + n] = (uint32_t)t;
+            }
+        have_adj = true;
+    }
+    int z = 0;
+    if (have_adj)
+        for (long long i = 0; i < q; ++i) z = std::max<int>(z, (int)(soff[i + 1] - soff[i]));
+    if (have_adj)
+        for (long long r = 0; r < m; ++r) rrec[r].w = (int)(soff[owner[r] + 1] - soff[owner[r]]);
+
+    const bool ell_from_matrix = e->format == SNP_FMT_ELL && !have_adj;
+    const bool dense_from_matrix = e->format == SNP_FMT_SPARSE && !have_adj;
+    if (e->format == SNP_FMT_COMPRESSED && !have_adj && q > 0)
+        return fail(SNP_ERR_BAD_ARG, "COMPRESSED needs adj_offsets/adj_targets or syn_target");
+    if (ell_from_matrix && m > 0 && !(d->ell_target && d->ell_amount))
+        return fail(SNP_ERR_BAD_ARG, "ELL needs adj_offsets/adj_targets or ell_target/ell_amount");
+    if (dense_from_matrix && m > 0 && q > 0 && !d->sparse_data)
+        return fail(SNP_ERR_BAD_ARG, "SPARSE needs adj_offsets/adj_targets or sparse_data");
+
+    std::vector<int2> ell_host;
+    std::vector<uint32_t> ell_len_host;
+    long long ell_ld = 0;
+    if (ell_from_matrix) {
+        const long long rows = d->ell_rows;
+        z = (int)std::max<long long>(0, rows - 1);
+        ell_ld = std::max<long long>(2, (rows + 1) & ~1ll);  // 16-byte aligned columns
+        ell_host.assign((size_t)(m * ell_ld), make_int2(-1, 0));
+        ell_len_host.assign(m, 0);
+        for (long long r = 0; r < m; ++r) {
+            long long n = 0;
+            while (n < rows && d->ell_target[n * m + r] >= 0) {
+                const long long t = d->ell_target[n * m + r], a = d->ell_amount[n * m + r];
+                if (t >= q) return fail(SNP_ERR_BAD_ARG, "ELL target %lld out of range", t);
+                if (a < -kInt32Max || a > kInt32Max) return fail(SNP_ERR_CAPACITY, "ELL amount %lld outside int32", a);
+                ell_host[r * ell_ld + n] = make_int2((int)t, (int)a);
+                ++n;
+            }
+            ell_len_host[r] = (uint32_t)n;
+            rrec[r].w = (int)std::max<long long>(0, n - 1);
+        }
+    }
+    e->z = z;
+
+    // --- receive path and P width
+    e->variant = d->variant;
+    if (e->format == SNP_FMT_COMPRESSED) {
+        if (e->variant == SNP_VARIANT_AUTO) e->variant = SNP_VARIANT_PULL;
+        e->kind = e->variant == SNP_VARIANT_PUSH ? RECV_ARRAY : RECV_PULL;
+    } else {
+        e->variant = SNP_VARIANT_PUSH;
+        e->kind = RECV_ARRAY;
+    }
+    if (pcommon) {
+        e->p_mode = P_BIT;
+        e->p_common = pfirst > 0 ? pfirst : 1;
+    } else if (pmax <= 255) {
+        e->p_mode = P_U8;
+    } else if (pmax <= 65535) {
+        e->p_mode = P_U16;
+    } else {
+        e->p_mode = P_U32;
+    }
+
+    CU(cudaSetDevice(e->device));
+    CU(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&e->ev0));
+    CU(cudaEventCreate(&e->ev1));
+
+    DevSys& s = e->sys;
+    DevState& st = e->st;
+    s.q = q;
+    s.m = m;
+    s.z = z;
+    s.ell_rows = z + 1;
+    s.p_common = e->p_common;
+    uint32_t* d_roff;
+    uint32_t* d_rthr;
+    int4* d_rrec;
+    TRY(upload(e, &d_roff, roff));
+    TRY(upload(e, &d_rthr, rthr));
+    TRY(upload(e, &d_rrec, rrec));
+    s.roff = d_roff;
+    s.rthr = d_rthr;
+    s.rrec = d_rrec;
+
+    uint32_t *d_soff = nullptr, *d_sdst = nullptr, *d_owner = nullptr;
+    const bool need_owner = (e->format != SNP_FMT_COMPRESSED && have_adj);
+    if (have_adj) {
+        TRY(upload(e, &d_soff, soff));
+        TRY(upload(e, &d_sdst, sdst));
+    }
+    if (need_owner) TRY(upload(e, &d_owner, owner));
+
+    // heavy list (CTA per neuron)
+    std::vector<uint32_t> indeg;
+    if (e->kind == RECV_PULL && q > 0) {
+        // in-adjacency = transpose of the out-adjacency, lists padded to x4
+        // with the sentinel source q (whose P entry is always 0)
+        uint32_t* d_indeg;
+        TRY(e->alloc(&d_indeg, q));
+        CU(cudaMemset(d_indeg, 0, q * sizeof(uint32_t)));
+        if (!sdst.empty()) {
+            indeg_kernel<<<std::min(grid_for((long long)sdst.size()), 148 * 64), 256>>>((long long)sdst.size(), d_sdst, d_indeg);
+            CU(cudaGetLastError());
+        }
+        indeg.resize(q);
+        CU(cudaMemcpy(indeg.data(), d_indeg, q * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> ioff(q + 1, 0);
+        unsigned long long acc = 0;
+        for (long long i = 0; i < q; ++i) {
+            ioff[i] = (uint32_t)acc;
+            acc += (indeg[i] + 3u) & ~3u;
+            if (acc >= (1ull << 32) - 4) return fail(SNP_ERR_CAPACITY, "in-adjacency exceeds uint32 offsets");
+        }
+        ioff[q] = (uint32_t)acc;
+        e->in_edges = (long long)acc;
+        uint32_t *d_ioff, *d_isrc, *d_cursor;
+        TRY(upload(e, &d_ioff, ioff));
+        TRY(e->alloc(&d_isrc, (long long)acc + 4));
+        fill_u32_kernel<<<std::min(grid_for((long long)acc + 4), 148 * 64), 256>>>((long long)acc + 4, d_isrc, (uint32_t)q);
+        CU(cudaGetLastError());
+        TRY(e->alloc(&d_cursor, q));
+        CU(cudaMemcpy(d_cursor, d_ioff, q * sizeof(uint32_t), cudaMemcpyDeviceToDevice));
+        transpose_fill_kernel<<<grid_for(q), 256>>>(q, d_soff, d_sdst, d_cursor, d_isrc);
+        CU(cudaGetLastError());
+        CU(cudaDeviceSynchronize());
+        s.ioff = d_ioff;
+        s.isrc = d_isrc;
+    }
+    std::vector<uint32_t> heavy;
+    for (long long i = 0; i < q; ++i) {
+        const bool many_rules = roff[i + 1] - roff[i] > kLightRules;
+        const bool many_in = e->kind == RECV_PULL && ((indeg[i] + 3u) & ~3u) > kLightIn;
+        if (many_rules || many_in) heavy.push_back((uint32_t)i);
+    }
+    uint32_t* d_heavy;
+    TRY(upload(e, &d_heavy, heavy));
+    s.heavy = d_heavy;
+    s.n_heavy = (int)heavy.size();
+    // at least one (possibly all-idle) light CTA so that q == 0 still runs
+    // the halting decision on the device
+    s.light_blocks = (int)std::max<long long>(1, ceil_div(q, kBlock));
+    e->step_grid = s.light_blocks + s.n_heavy;
+
+    if (e->format == SNP_FMT_COMPRESSED && e->kind == RECV_ARRAY) {
+        s.soff = d_soff;
+        s.sdst = d_sdst;
+    }
+    if (e->format == SNP_FMT_ELL) {
+        uint32_t* d_len;
+        int2* d_ell;
+        if (ell_from_matrix) {
+            TRY(upload(e, &d_ell, ell_host));
+            TRY(upload(e, &d_len, ell_len_host));
+        } else {
+            ell_ld = std::max<long long>(2, (z + 2) & ~1ll);
+            TRY(e->alloc(&d_ell, m * ell_ld));
+            TRY(e->alloc(&d_len, m));
+            CU(cudaMemset(d_ell, 0xff, (size_t)std::max<long long>(1, m * ell_ld) * sizeof(int2)));
+            if (m > 0) build_ell_kernel<<<grid_for(m), 256>>>(m, ell_ld, d_owner, d_rrec, d_soff, d_sdst, d_ell, d_len);
+            CU(cudaGetLastError());
+        }
+        s.ell = d_ell;
+        s.ell_len = d_len;
+        s.ell_ld = ell_ld;
+    }
+    if (e->format == SNP_FMT_SPARSE) {
+        const long long ld = std::max<long long>(4, (q + 3) & ~3ll);
+        int* d_dense;
+        if ((double)m * (double)ld * 4.0 > 9.0e18) return fail(SNP_ERR_CAPACITY, "dense matrix too large");
+        TRY(e->alloc(&d_dense, m * ld));
+        CU(cudaMemset(d_dense, 0, (size_t)std::max<long long>(1, m * ld) * sizeof(int)));
+        if (dense_from_matrix) {
+            std::vector<int> row(ld, 0);
+            for (long long r = 0; r < m; ++r) {
+                for (long long i = 0; i < q; ++i) {
+                    const long long v = d->sparse_data[r * q + i];
+                    if (v < -kInt32Max || v > kInt32Max) return fail(SNP_ERR_CAPACITY, "dense entry outside int32");
+                    row[i] = (int)v;
+                }
+                CU(cudaMemcpy(d_dense + r * ld, row.data(), ld * sizeof(int), cudaMemcpyHostToDevice));
+            }
+        } else if (m > 0) {
+            build_dense_kernel<<<grid_for(m), 256>>>(m, ld, d_owner, d_rrec, d_soff, d_sdst, d_dense);
+            CU(cudaGetLastError());
+        }
+        s.dense = d_dense;
+        s.dense_ld = ld;
+        const int col_tiles = (int)std::max<long long>(1, ceil_div(q, kBlock * 4));
+        const int splits = std::max(1, std::min(1024, 148 * 8 / col_tiles));
+        e->dense_grid = dim3(col_tiles, splits, 1);
+    }
+
+    // --- run state
+    TRY(e->alloc(&st.cfg, q));
+    TRY(e->alloc(&st.ds, q));
+    TRY(e->alloc(&st.chosen, q));
+    if (e->kind == RECV_PULL) {
+        long long words;
+        switch (e->p_mode) {
+            case P_BIT: words = ceil_div(q + 1, 32) + 1; break;
+            case P_U8: words = ceil_div(q + 1, 4) + 1; break;
+            case P_U16: words = ceil_div(q + 1, 2) + 1; break;
+            default: words = q + 2; break;
+        }
+        for (int i = 0; i < 3; ++i) TRY(e->alloc(&st.P[i], words));
+    } else {
+        TRY(e->alloc(&st.recv, q));
+        TRY(e->alloc(&st.list[0], q));
+        TRY(e->alloc(&st.list[1], q));
+    }
+    TRY(e->alloc(&st.ctrl, 1));
+    e->push_grid = grid_for(q);
+    e->heavy_push_grid = 148 * 4;
+
+    // kernel instances
+    if (e->format == SNP_FMT_COMPRESSED && e->kind == RECV_PULL) {
+        switch (e->p_mode) {
+            case P_BIT: pick_fns<RECV_PULL, P_BIT, true, false>(&e->step_fn, &e->prime_fn); break;
+            case P_U8: pick_fns<RECV_PULL, P_U8, true, false>(&e->step_fn, &e->prime_fn); break;
+            case P_U16: pick_fns<RECV_PULL, P_U16, true, false>(&e->step_fn, &e->prime_fn); break;
+            default: pick_fns<RECV_PULL, P_U32, true, false>(&e->step_fn, &e->prime_fn); break;
+        }
+    } else if (e->format == SNP_FMT_COMPRESSED) {
+        pick_fns<RECV_ARRAY, P_BIT, true, false>(&e->step_fn, &e->prime_fn);
+    } else if (e->format == SNP_FMT_ELL) {
+        pick_fns<RECV_ARRAY, P_BIT, false, false>(&e->step_fn, &e->prime_fn);
+    } else {
+        pick_fns<RECV_ARRAY, P_BIT, false, true>(&e->step_fn, &e->prime_fn);
+    }
+    CU(cudaDeviceSynchronize());
+    return SNP_OK;
+}
+
+// Launch one step's kernels on the engine stream; returns launch count.
+int launch_step(snp_engine* e, long long* row_visits = nullptr) {
+    int n = 1;
+    e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+    if (e->kind == RECV_ARRAY) {
+        if (e->format == SNP_FMT_SPARSE) {
+            dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+            n += 1;
+        } else if (e->format == SNP_FMT_ELL) {
+            push_kernel<true><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, row_visits);
+            push_heavy_kernel<true><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+            n += 2;
+        } else {
+            push_kernel<false><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, row_visits);
+            push_heavy_kernel<false><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+            n += 2;
+        }
+    }
+    return n;
+}
+
+int push_ctrl(snp_engine* e) {
+    CU(cudaMemcpyAsync(e->st.ctrl, &e->hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    return SNP_OK;
+}
+
+int pull_ctrl(snp_engine* e) {
+    CU(cudaMemcpyAsync(&e->hctrl, e->st.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    return SNP_OK;
+}
+
+int reset_state(snp_engine* e) {
+    const long long q = e->q;
+    DevState& st = e->st;
+    if (e->kind == RECV_PULL) {
+        // all three P vectors start empty: P_{-1} = 0 and the bit words are
+        // OR-accumulated into zeroed buffers
+        for (int i = 0; i < 3; ++i) {
+            size_t bytes;
+            switch (e->p_mode) {
+                case P_BIT: bytes = (ceil_div(q + 1, 32) + 1) * 4; break;
+                case P_U8: bytes = (ceil_div(q + 1, 4) + 1) * 4; break;
+                case P_U16: bytes = (ceil_div(q + 1, 2) + 1) * 4; break;
+                default: bytes = (q + 2) * 4; break;
+            }
+            CU(cudaMemsetAsync(st.P[i], 0, bytes, e->stream));
+        }
+    } else {
+        CU(cudaMemsetAsync(st.recv, 0, std::max<long long>(1, q) * 8, e->stream));
+    }
+    CU(cudaMemsetAsync(st.ds, 0, std::max<long long>(1, q) * 4, e->stream));
+    CU(cudaMemsetAsync(st.chosen, 0xff, std::max<long long>(1, q) * 4, e->stream));
+    memset(&e->hctrl, 0, sizeof(Ctrl));
+    e->hctrl.neg_index = 0x7fffffffffffffffll;
+    e->hctrl.max_steps = 1;
+    return SNP_OK;
+}
+
+int ensure_trace(snp_engine* e, long long rows) {
+    if (e->tr_rows >= rows) return SNP_OK;
+    // (re)allocate the ring; the graph captures its pointers
+    long long* cfg;
+    int *dly, *ch;
+    TRY(e->alloc(&cfg, rows * std::max<long long>(1, e->q)));
+    TRY(e->alloc(&dly, rows * std::max<long long>(1, e->q)));
+    TRY(e->alloc(&ch, rows * std::max<long long>(1, e->q)));
+    e->st.tr_cfg = cfg;
+    e->st.tr_dly = dly;
+    e->st.tr_chosen = ch;
+    e->st.tr_rows = rows;
+    e->tr_rows = rows;
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    return SNP_OK;
+}
+
+int ensure_graph(snp_engine* e, long long iters) {
+    if (e->graph && e->graph_iters == iters) return SNP_OK;
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    for (long long i = 0; i < iters; ++i) launch_step(e);
+    CU(cudaStreamEndCapture(e->stream, &g));
+    cudaError_t err = cudaGraphInstantiate(&e->graph, g, 0);
+    cudaGraphDestroy(g);
+    CU(err);
+    e->graph_iters = iters;
+    return SNP_OK;
+}
+
+int kernels_per_step(const snp_engine* e) {
+    if (e->kind == RECV_PULL) return 1;
+    return e->format == SNP_FMT_SPARSE ? 2 : 3;
+}
+
+int validate_opts(const snp_run_opts* o) {
+    if (!o) return fail(SNP_ERR_BAD_ARG, "options missing");
+    if (o->max_steps < 1) return fail(SNP_ERR_BAD_ARG, "max_steps must be >= 1, got %lld", (long long)o->max_steps);
+    if (o->policy != SNP_POLICY_FIRST && o->policy != SNP_POLICY_SEEDED)
+        return fail(SNP_ERR_BAD_ARG, "unknown policy %d", o->policy);
+    if (o->record & ~7) return fail(SNP_ERR_BAD_ARG, "bad record flags %d", o->record);
+    return SNP_OK;
+}
+
+void fill_result(const snp_engine* e, snp_result* res) {
+    if (!res) return;
+    const Ctrl& c = e->hctrl;
+    res->steps = c.step;
+    res->halt = c.halted ? c.reason : SNP_RUNNING;
+    res->error = (c.halted && c.reason == HALT_NEGATIVE) ? SNP_ERR_NEGATIVE : SNP_OK;
+    res->negative_neuron = c.neg_any ? c.neg_index : -1;
+    res->negative_value = c.neg_any ? c.neg_value : 0;
+    for (int i = 0; i < SNP_STAT_COUNT; ++i) res->stats[i] = c.stats[i];
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+int snp_abi_version(void) { return SNPB200_ABI_VERSION; }
+
+const char* snp_last_error(void) { return g_last_error.c_str(); }
+
+int snp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
+    if (!desc || !out) return fail(SNP_ERR_BAD_ARG, "null argument");
+    if (desc->format < SNP_FMT_SPARSE || desc->format > SNP_FMT_COMPRESSED)
+        return fail(SNP_ERR_BAD_ARG, "unknown format %d", desc->format);
+    if (snp_device_count() <= desc->device)
+        return fail(SNP_ERR_CUDA, "no CUDA device %d visible (the B200 engine has no CPU fallback)", desc->device);
+    auto e = std::make_unique<snp_engine>();
+    e->device = desc->device;
+    int rc = build(e.get(), desc);
+    if (rc != SNP_OK) return rc;
+    *out = e.release();
+    return SNP_OK;
+}
+
+void snp_engine_destroy(snp_engine* eng) {
+    if (!eng) return;
+    cudaSetDevice(eng->device);
+    delete eng;
+}
+
+int snp_engine_get_info(const snp_engine* e, snp_engine_info* info) {
+    if (!e || !info) return fail(SNP_ERR_BAD_ARG, "null argument");
+    info->q = e->q;
+    info->m = e->m;
+    info->z = e->z;
+    info->device_bytes = e->device_bytes;
+    info->format = e->format;
+    info->variant = e->variant;
+    info->p_mode = e->p_mode;
+    info->heavy_neurons = e->sys.n_heavy;
+    info->in_edges = e->in_edges;
+    info->p_common = e->p_common;
+    return SNP_OK;
+}
+
+int snp_begin(snp_engine* e, const int64_t* initial) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    CU(cudaSetDevice(e->device));
+    TRY(reset_state(e));
+    const long long q = e->q;
+    const long long* src = initial ? reinterpret_cast<const long long*>(initial) : e->initial.data();
+    if (q > 0) CU(cudaMemcpyAsync(e->st.cfg, src, q * 8, cudaMemcpyHostToDevice, e->stream));
+    TRY(push_ctrl(e));
+    CU(cudaStreamSynchronize(e->stream));
+    e->begun = true;
+    return SNP_OK;
+}
+
+int snp_advance(snp_engine* e, const snp_run_opts* o, int64_t n_steps, snp_trace_out* tr, snp_result* res) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    TRY(validate_opts(o));
+    if (!e->begun) return fail(SNP_ERR_BAD_ARG, "snp_advance before snp_begin");
+    CU(cudaSetDevice(e->device));
+    const long long q = e->q;
+    const int record = tr ? o->record : 0;
+    long long chunk = o->chunk > 0 ? o->chunk : (q >= (1ll << 20) ? 16 : (q >= (1ll << 14) ? 64 : 256));
+    if (record) {
+        long long budget_rows = std::max<long long>(1, (1ll << 30) / std::max<long long>(1, q * 16));
+        chunk = std::min(chunk, budget_rows);
+        if (tr->cap < 1) return fail(SNP_ERR_BAD_ARG, "trace capacity must be >= 1");
+        chunk = std::min<long long>(chunk, tr->cap);
+        TRY(ensure_trace(e, chunk));
+    }
+    if (tr) {
+        tr->first_row_step = e->hctrl.step;
+        tr->config_rows = 0;
+        tr->spiking_rows = 0;
+    }
+    Ctrl& c = e->hctrl;
+    c.max_steps = o->max_steps;
+    c.policy = o->policy;
+    c.seed = o->seed;
+    c.record = record;
+    c.stats_on = o->collect_stats ? 1 : 0;
+    long long budget = (long long)n_steps;
+    long long launches = 0;
+    std::vector<int> tmp;
+    CU(cudaEventRecord(e->ev0, e->stream));
+    while (budget > 0 && !c.halted) {
+        long long seg = std::min(chunk, budget);
+        if (record) seg = std::min<long long>(seg, (long long)(tr->cap - tr->config_rows));
+        if (seg <= 0) break;
+        const long long k0 = c.step;
+        c.stop_at = k0 + seg;
+        c.trace_base = k0;
+        TRY(push_ctrl(e));
+        if (o->use_graph) {
+            TRY(ensure_graph(e, chunk));
+            CU(cudaGraphLaunch(e->graph, e->stream));
+            launches += chunk * kernels_per_step(e);
+        } else {
+            for (long long i = 0; i < seg; ++i) launches += launch_step(e);
+            CU(cudaGetLastError());
+        }
+        TRY(pull_ctrl(e));
+        const long long k1 = c.halted ? c.step : c.step;  // halt step or next step
+        long long cfg_rows = c.halted ? (k1 - k0 + 1) : (k1 - k0);
+        long long sp_rows = k1 - k0;
+        if (c.halted && c.reason == HALT_NEGATIVE) break;
+        if (record && cfg_rows > 0) {
+            const long long r0 = tr->config_rows;
+            if (tr->configs && (record & REC_CONFIGS))
+                CU(cudaMemcpy(tr->configs + r0 * q, e->st.tr_cfg, cfg_rows * q * 8, cudaMemcpyDeviceToHost));
+            if (tr->delays && (record & REC_DELAYS)) {
+                tmp.resize((size_t)(cfg_rows * q));
+                CU(cudaMemcpy(tmp.data(), e->st.tr_dly, cfg_rows * q * 4, cudaMemcpyDeviceToHost));
+                for (long long i = 0; i < cfg_rows * q; ++i) tr->delays[r0 * q + i] = tmp[i];
+            }
+            if (tr->spiking && (record & REC_SPIKING) && sp_rows > 0) {
+                tmp.resize((size_t)(sp_rows * q));
+                CU(cudaMemcpy(tmp.data(), e->st.tr_chosen, sp_rows * q * 4, cudaMemcpyDeviceToHost));
+                const long long s0 = tr->spiking_rows;
+                for (long long i = 0; i < sp_rows * q; ++i) tr->spiking[s0 * q + i] = tmp[i];
+            }
+            tr->config_rows += cfg_rows;
+            tr->spiking_rows += sp_rows;
+        }
+        budget -= (k1 - k0) + (c.halted ? 1 : 0);
+    }
+    CU(cudaEventRecord(e->ev1, e->stream));
+    CU(cudaEventSynchronize(e->ev1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->last_ms = ms;
+    fill_result(e, res);
+    if (res) res->kernel_launches = launches;
+    if (c.halted && c.reason == HALT_NEGATIVE)
+        return fail(SNP_ERR_NEGATIVE, "spike counts went negative (neuron %lld: %lld); the applied rule consumed more than stored",
+                    c.neg_index, c.neg_value);
+    return SNP_OK;
+}
+
+int snp_read_state(snp_engine* e, int64_t* config, int64_t* delays) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    if (!e->hctrl.halted) return fail(SNP_ERR_BAD_ARG, "snp_read_state needs a halted run");
+    CU(cudaSetDevice(e->device));
+    const long long q = e->q;
+    if (q == 0) return SNP_OK;
+    if (config) CU(cudaMemcpy(config, e->st.cfg, q * 8, cudaMemcpyDeviceToHost));
+    if (delays) {
+        if (!e->scratch[0]) TRY(e->alloc(&e->scratch[0], q));
+        ds_to_delay_kernel<<<grid_for(q), 256, 0, e->stream>>>(q, e->st.ds, e->scratch[0]);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(delays, e->scratch[0], q * 8, cudaMemcpyDeviceToHost, e->stream));
+        CU(cudaStreamSynchronize(e->stream));
+    }
+    return SNP_OK;
+}
+
+int snp_run(snp_engine* e, const int64_t* initial, const snp_run_opts* o, int64_t* final_config,
+            int64_t* final_delays, snp_result* res) {
+    TRY(validate_opts(o));
+    TRY(snp_begin(e, initial));
+    TRY(snp_advance(e, o, o->max_steps + 1, nullptr, res));
+    return snp_read_state(e, final_config, final_delays);
+}
+
+double snp_last_device_ms(const snp_engine* e) { return e ? e->last_ms : 0.0; }
+
+int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* total_ms, double* kernel_ms,
+                   snp_result* res) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    TRY(validate_opts(o));
+    if (!e->begun) return fail(SNP_ERR_BAD_ARG, "snp_time_steps before snp_begin");
+    CU(cudaSetDevice(e->device));
+    Ctrl& c = e->hctrl;
+    c.max_steps = o->max_steps;
+    c.policy = o->policy;
+    c.seed = o->seed;
+    c.record = 0;
+    c.stats_on = o->collect_stats ? 1 : 0;
+    c.stop_at = c.step + steps;
+    TRY(push_ctrl(e));
+    long long launches = 0;
+    if (kernel_ms) {
+        // per-kernel CUDA events around the step kernel on the engine stream
+        std::vector<cudaEvent_t> ev(2 * steps);
+        for (auto& x : ev) CU(cudaEventCreate(&x));
+        CU(cudaEventRecord(e->ev0, e->stream));
+        for (long long i = 0; i < steps; ++i) {
+            CU(cudaEventRecord(ev[2 * i], e->stream));
+            e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+            CU(cudaEventRecord(ev[2 * i + 1], e->stream));
+            launches += 1;
+            if (e->kind == RECV_ARRAY) {
+                // push kernels of the same step, launched after the timed one
+                if (e->format == SNP_FMT_SPARSE) {
+                    dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+                    launches += 1;
+                } else if (e->format == SNP_FMT_ELL) {
+                    push_kernel<true><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, nullptr);
+                    push_heavy_kernel<true><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+                    launches += 2;
+                } else {
+                    push_kernel<false><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, nullptr);
+                    push_heavy_kernel<false><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+                    launches += 2;
+                }
+            }
+        }
+        CU(cudaEventRecord(e->ev1, e->stream));
+        CU(cudaEventSynchronize(e->ev1));
+        double sum = 0;
+        for (long long i = 0; i < steps; ++i) {
+            float ms = 0;
+            CU(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+            sum += ms;
+        }
+        for (auto& x : ev) cudaEventDestroy(x);
+        *kernel_ms = steps > 0 ? sum / steps : 0.0;
+    } else {
+        const long long chunk = std::min<long long>((long long)steps, 64ll);
+        TRY(ensure_graph(e, chunk));
+        CU(cudaEventRecord(e->ev0, e->stream));
+        long long done = 0;
+        while (done < steps) {
+            CU(cudaGraphLaunch(e->graph, e->stream));
+            launches += chunk * kernels_per_step(e);
+            done += chunk;
+        }
+        CU(cudaEventRecord(e->ev1, e->stream));
+        CU(cudaEventSynchronize(e->ev1));
+    }
+    float tot = 0;
+    CU(cudaEventElapsedTime(&tot, e->ev0, e->ev1));
+    if (total_ms) *total_ms = tot;
+    e->last_ms = tot;
+    TRY(pull_ctrl(e));
+    fill_result(e, res);
+    if (res) res->kernel_launches = launches;
+    if (c.halted && c.reason == HALT_NEGATIVE) return fail(SNP_ERR_NEGATIVE, "spike counts went negative");
+    return SNP_OK;
+}
+
+// --------------------------------------------------------------- phase API
+
+static int phase_scratch(snp_engine* e) {
+    for (int i = 0; i < 4; ++i)
+        if (!e->scratch[i]) TRY(e->alloc(&e->scratch[i], std::max<long long>(1, e->q)));
+    return SNP_OK;
+}
+
+int snp_sv_calc(snp_engine* e, const int64_t* config, const int64_t* delays, int32_t policy, uint64_t seed,
+                int64_t step, int64_t* chosen) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    if (policy != SNP_POLICY_FIRST && policy != SNP_POLICY_SEEDED) return fail(SNP_ERR_BAD_ARG, "unknown policy");
+    if (step < 0) return fail(SNP_ERR_BAD_ARG, "step must be >= 0");
+    CU(cudaSetDevice(e->device));
+    const long long q = e->q;
+    for (long long i = 0; i < q; ++i)
+        if (delays[i] < 0 || delays[i] > kInt32Max - 2) return fail(SNP_ERR_BAD_ARG, "delay out of range");
+    TRY(phase_scratch(e));
+    TRY(ensure_trace(e, std::max<long long>(1, e->tr_rows)));
+    TRY(reset_state(e));
+    if (q > 0) {
+        CU(cudaMemcpyAsync(e->scratch[0], config, q * 8, cudaMemcpyHostToDevice, e->stream));
+        CU(cudaMemcpyAsync(e->scratch[1], delays, q * 8, cudaMemcpyHostToDevice, e->stream));
+        load_state_kernel<<<grid_for(q), 256, 0, e->stream>>>(q, e->st.cfg, e->st.ds, e->scratch[0], e->scratch[1]);
+        CU(cudaGetLastError());
+    }
+    Ctrl& c = e->hctrl;
+    c.step = step;
+    c.max_steps = step + 1;
+    c.stop_at = step + 1;
+    c.trace_base = step;
+    c.policy = policy;
+    c.seed = seed;
+    c.record = REC_SPIKING;
+    TRY(push_ctrl(e));
+    e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+    CU(cudaGetLastError());
+    if (q > 0) {
+        widen_i32_kernel<<<grid_for(q), 256, 0, e->stream>>>(q, e->st.tr_chosen, e->scratch[2]);
+        CU(cudaMemcpyAsync(chosen, e->scratch[2], q * 8, cudaMemcpyDeviceToHost, e->stream));
+    }
+    TRY(pull_ctrl(e));
+    e->begun = false;
+    return SNP_OK;
+}
+
+int snp_step(snp_engine* e, const int64_t* config, const int64_t* delays, const int64_t* chosen,
+             int64_t* next_config, int64_t* row_visits) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    CU(cudaSetDevice(e->device));
+    const long long q = e->q, m = e->m;
+    for (long long i = 0; i < q; ++i) {
+        if (delays[i] < 0 || delays[i] > kInt32Max - 2) return fail(SNP_ERR_BAD_ARG, "delay out of range");
+        if (chosen[i] < -1 || chosen[i] >= m) return fail(SNP_ERR_BAD_ARG, "chosen rule %lld out of range", (long long)chosen[i]);
+    }
+    TRY(phase_scratch(e));
+    TRY(reset_state(e));
+    long long* d_visits = nullptr;
+    if (row_visits && e->format == SNP_FMT_ELL && m > 0) {
+        TRY(e->alloc(&d_visits, m));
+        CU(cudaMemcpyAsync(d_visits, row_visits, m * 8, cudaMemcpyHostToDevice, e->stream));
+    }
+    if (q > 0) {
+        CU(cudaMemcpyAsync(e->scratch[0], config, q * 8, cudaMemcpyHostToDevice, e->stream));
+        CU(cudaMemcpyAsync(e->scratch[1], delays, q * 8, cudaMemcpyHostToDevice, e->stream));
+        CU(cudaMemcpyAsync(e->scratch[2], chosen, q * 8, cudaMemcpyHostToDevice, e->stream));
+    }
+    Ctrl& c = e->hctrl;
+    c.step = 1;  // the prime kernel plays "step 0's selection"
+    c.max_steps = 1;
+    c.stop_at = 2;
+    c.trace_base = 1;
+    c.record = 0;
+    c.push_armed = 1;
+    TRY(push_ctrl(e));
+    if (q > 0) {
+        e->prime_fn<<<grid_for(q), 256, 0, e->stream>>>(e->sys, e->st, e->scratch[0], e->scratch[1], e->scratch[2]);
+        CU(cudaGetLastError());
+    }
+    if (e->kind == RECV_ARRAY) {
+        if (e->format == SNP_FMT_SPARSE) {
+            dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+        } else if (e->format == SNP_FMT_ELL) {
+            push_kernel<true><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, d_visits);
+            push_heavy_kernel<true><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+        } else {
+            push_kernel<false><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, nullptr);
+            push_heavy_kernel<false><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+        }
+        CU(cudaGetLastError());
+    }
+    e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);  // finalize only
+    CU(cudaGetLastError());
+    TRY(pull_ctrl(e));
+    e->begun = false;
+    if (c.halted && c.reason == HALT_NEGATIVE)
+        return fail(SNP_ERR_NEGATIVE, "spike counts went negative (neuron %lld: %lld); the applied rule consumed more than stored",
+                    c.neg_index, c.neg_value);
+    if (q > 0) CU(cudaMemcpy(next_config, e->st.cfg, q * 8, cudaMemcpyDeviceToHost));
+    if (d_visits) CU(cudaMemcpy(row_visits, d_visits, m * 8, cudaMemcpyDeviceToHost));
+    return SNP_OK;
+}
+
+int snp_update_delays(snp_engine* e, const int64_t* delays, const int64_t* chosen, int64_t* next_delays) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    CU(cudaSetDevice(e->device));
+    const long long q = e->q;
+    for (long long i = 0; i < q; ++i)
+        if (chosen[i] < -1 || chosen[i] >= e->m) return fail(SNP_ERR_BAD_ARG, "chosen rule out of range");
+    if (q == 0) return SNP_OK;
+    TRY(phase_scratch(e));
+    CU(cudaMemcpyAsync(e->scratch[0], delays, q * 8, cudaMemcpyHostToDevice, e->stream));
+    CU(cudaMemcpyAsync(e->scratch[1], chosen, q * 8, cudaMemcpyHostToDevice, e->stream));
+    update_delays_kernel<<<grid_for(q), 256, 0, e->stream>>>(q, e->sys.rrec, e->scratch[0], e->scratch[1], e->scratch[2]);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(next_delays, e->scratch[2], q * 8, cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    return SNP_OK;
+}
+
+}  // extern "C"

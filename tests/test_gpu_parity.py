@@ -1,0 +1,314 @@
+"""B200 engine vs the reference (golden fixtures) and the pinned CPU oracle.
+
+Every test here runs the CUDA kernels through the C ABI (libsnpb200.so) and
+requires bit-exact equality: configurations, delays, spiking vectors (global
+rule ids) and halting step/reason at every step.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2408_04343_b200 as snp
+from conftest import (corpus_size, corpus_system, golden_npz, scenario_names, scenario_system,
+                      scenario_trace, to_system_arrays)
+from oracle import coracle
+from oracle.snp_oracle import OracleSystem, trace_digest
+
+pytestmark = pytest.mark.gpu
+
+FORMATS = [(snp.Format.SPARSE, "auto"), (snp.Format.ELL, "auto"), (snp.Format.COMPRESSED, "pull"),
+           (snp.Format.COMPRESSED, "push")]
+FMT_IDS = ["sparse", "ell", "compressed-pull", "compressed-push"]
+POLICIES = {"first": snp.FirstApplicable(), "seeded7": snp.SeededRandom(7),
+            "seeded_big": snp.SeededRandom(2**63 + 5)}
+
+
+def _check(trace, gold):
+    assert trace.halt_reason.value == str(gold["halt"])
+    np.testing.assert_array_equal(np.stack(trace.configs), gold["configs"])
+    if "delays" in gold:
+        np.testing.assert_array_equal(np.stack(trace.delays), gold["delays"])
+    if "spiking" in gold:
+        q = gold["configs"].shape[1]
+        sp = np.stack(trace.spiking) if trace.spiking else np.zeros((0, q), np.int64)
+        np.testing.assert_array_equal(sp, gold["spiking"])
+
+
+# -- whole-run traces vs the reference ----------------------------------------------------
+
+@pytest.mark.parametrize("fmt,variant", FORMATS, ids=FMT_IDS)
+@pytest.mark.parametrize("name", scenario_names())
+def test_scenarios_match_reference(fmt, variant, name):
+    prep = snp.prepare(to_system_arrays(scenario_system(name)), fmt, variant=variant)
+    for tag, sel in POLICIES.items():
+        tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=60, selection=sel,
+                                                        record=snp.RecordLevel.FULL))
+        _check(tr, scenario_trace(name, tag))
+
+
+@pytest.mark.parametrize("fmt,variant", FORMATS, ids=FMT_IDS)
+def test_corpus_matches_reference_digests(fmt, variant):
+    """C3 (test_acceptance.py:151-167): 1000 random systems x 2 policies,
+    L=100, FULL traces identical to the reference (sha256 of every row)."""
+    c = golden_npz("corpus.npz")
+    L = int(c["L"])
+    n = corpus_size() if (fmt is snp.Format.COMPRESSED and variant == "pull") else 400
+    for i in range(n):
+        prep = snp.prepare(to_system_arrays(corpus_system(i)), fmt, variant=variant)
+        for sel, key in ((snp.FirstApplicable(), "first"), (snp.SeededRandom(i), "seeded")):
+            tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=L, selection=sel,
+                                                            record=snp.RecordLevel.FULL))
+            assert trace_digest(tr.configs, tr.delays, tr.spiking) == c[f"digest_{key}"][i], (i, key)
+
+
+@pytest.mark.parametrize("tag", ["k3", "k4"])
+@pytest.mark.parametrize("fmt,variant", FORMATS, ids=FMT_IDS)
+def test_synth_matches_reference(tag, fmt, variant):
+    d = golden_npz("synth.npz")
+    a = snp.synth_v1(int(d[f"{tag}/q"]), with_delays=bool(d[f"{tag}/delays"]))
+    prep = snp.prepare(a, fmt, variant=variant)
+    for pol, sel in (("first", snp.FirstApplicable()), ("seeded", snp.SeededRandom(99))):
+        gold = {k.split("/")[-1]: d[k] for k in d if k.startswith(f"{tag}/{pol}/")}
+        tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=int(d["steps"]), selection=sel,
+                                                        record=snp.RecordLevel.FULL))
+        _check(tr, gold)
+
+
+def test_synth_20k_digest():
+    d = golden_npz("synth.npz")
+    prep = snp.prepare(snp.synth_v1(int(d["k3big/q"])), snp.Format.COMPRESSED)
+    for pol, sel in (("first", snp.FirstApplicable()), ("seeded", snp.SeededRandom(99))):
+        tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=int(d["steps"]), selection=sel,
+                                                        record=snp.RecordLevel.FULL))
+        assert trace_digest(tr.configs, tr.delays, tr.spiking) == str(d[f"k3big/{pol}/digest"])
+
+
+# -- sort family (test_acceptance.py:170-183; section 6) -------------------------
+
+@pytest.mark.parametrize("fmt,variant", FORMATS, ids=FMT_IDS)
+@pytest.mark.parametrize("n", [3, 5, 10, 100])
+def test_sorting_end_to_end(fmt, variant, n):
+    prep = snp.prepare(snp.gen_sort(snp.SortInstance(n)), fmt, variant=variant)
+    tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=n + 10))
+    assert tr.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
+    assert snp.sort_result(tr, n) == list(range(1, n + 1))
+    if n == 100:
+        t = golden_npz("traces.npz")
+        assert trace_digest(tr.configs) == str(t["sort100/digest"])
+
+
+@pytest.mark.parametrize("n,fmts", [(512, FORMATS), (2048, [(snp.Format.COMPRESSED, "pull"),
+                                                            (snp.Format.COMPRESSED, "push")])])
+def test_sort_large_halts_sorted(n, fmts):
+    """Heavy-neuron path (detectors own n rules and n in-neighbours)."""
+    rng = np.random.default_rng(n)
+    values = tuple(int(v) for v in rng.choice(np.arange(1, 4 * n), size=n, replace=False))
+    a = snp.sort_arrays(snp.SortInstance(n, values))
+    want_final = None
+    for fmt, variant in fmts:
+        prep = snp.prepare(a, fmt, variant=variant)
+        res = snp.run_final(prep, snp.SimOptions(max_steps=5 * n))
+        assert res.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
+        assert res.config[2 * n:].tolist() == sorted(values)
+        if want_final is None:
+            want_final = res.config
+        np.testing.assert_array_equal(res.config, want_final)
+    # the first 40 steps are bit-exact against the C oracle
+    tr, _, _ = coracle.run(OracleSystem.from_arrays(a), 40, trace_rows=41)
+    prep = snp.prepare(a, snp.Format.COMPRESSED)
+    mine = snp.simulate_prepared(prep, snp.SimOptions(max_steps=40, record=snp.RecordLevel.FULL))
+    assert trace_digest(mine.configs, mine.delays, mine.spiking) == trace_digest(tr.configs, tr.delays, tr.spiking)
+
+
+def test_subset_sum_accepting_paths():
+    t = golden_npz("traces.npz")
+    prep = snp.prepare(to_system_arrays(scenario_system("subset12")), snp.Format.COMPRESSED)
+    adder = scenario_system("subset12").q - 1
+    got = [int(snp.run_final(prep, snp.SimOptions(max_steps=6, selection=snp.SeededRandom(s))).config[adder])
+           for s in range(200)]
+    assert got == t["subset12/accept_final_adder"].tolist()
+    assert 0 in got  # some seed accepts
+
+
+# -- full-size parity (K3 / K4 at 10^7 against the C oracle) ------------------------------
+
+@pytest.mark.parametrize("delays,policy", [(False, 0), (True, 1)])
+def test_full_size_synth_steps_bit_exact(delays, policy):
+    q, steps = 10_000_000, 3
+    a = snp.synth_v1(q, with_delays=delays)
+    sel = snp.FirstApplicable() if policy == 0 else snp.SeededRandom(240804343)
+    seed = 0 if policy == 0 else 240804343
+    prep = snp.prepare(a, snp.Format.COMPRESSED)
+    res = snp.run_final(prep, snp.SimOptions(max_steps=steps, selection=sel))
+    _, want_c, want_d = coracle.run(OracleSystem.from_arrays(a), steps, policy, seed)
+    np.testing.assert_array_equal(res.config, want_c)
+    np.testing.assert_array_equal(res.delays, want_d)
+    assert res.steps == steps and res.halt_reason is snp.HaltReason.STEP_LIMIT
+
+
+def test_full_size_formats_agree():
+    """ELL and push-Optimized reach the same state as pull-Optimized at 10^7."""
+    a = snp.synth_v1(10_000_000, with_delays=True)
+    finals = []
+    for fmt, variant in [(snp.Format.COMPRESSED, "pull"), (snp.Format.COMPRESSED, "push"), (snp.Format.ELL, "auto")]:
+        prep = snp.prepare(a, fmt, variant=variant)
+        finals.append(snp.run_final(prep, snp.SimOptions(max_steps=4)).config)
+        del prep
+    np.testing.assert_array_equal(finals[0], finals[1])
+    np.testing.assert_array_equal(finals[0], finals[2])
+
+
+# -- phase functions (test_engine.py:66-259) --------------------------------------------------
+
+def _relay(c=2, p=1, d=0):
+    s = snp.SNPSystem()
+    a, b = s.add_neuron(2), s.add_neuron(0)
+    s.add_rule(a, snp.at_least(c), c, p, d)
+    s.add_synapse(a, b)
+    return s.validate()
+
+
+def test_sv_calc_sorter_detector():
+    system = snp.gen_sort(snp.SortInstance(3))
+    rules, rm = snp.build_rule_vector(system)
+    cfg = np.zeros(9, dtype=np.int64)
+    cfg[3] = 3
+    sv = snp.sv_calc(cfg, np.zeros(9, dtype=np.int64), rules, rm, snp.FirstApplicable())
+    assert sv.chosen[3] == 3 and sv.flags(12).sum() == 1
+
+
+def test_sv_calc_closed_and_first_applicable():
+    system = _relay()
+    rules, rm = snp.build_rule_vector(system)
+    sv = snp.sv_calc(np.array([2, 0]), np.array([1, 2]), rules, rm, snp.FirstApplicable())
+    assert sv.is_empty
+    s = snp.SNPSystem()
+    a = s.add_neuron(2)
+    s.add_rule(a, snp.exactly(2), 2, 1, 0)
+    s.add_rule(a, snp.at_least(1), 1, 1, 0)
+    s.validate()
+    rules, rm = snp.build_rule_vector(s)
+    assert snp.sv_calc(np.array([2]), np.zeros(1, np.int64), rules, rm, snp.FirstApplicable()).chosen[0] == 0
+    # seeded: roughly uniform over seeds (test_engine.py:97-111), exactly the reference's picks
+    from paper_2408_04343_b200.selection import mix64
+    first = 0
+    for seed in range(2000):
+        ch = snp.sv_calc(np.array([2]), np.zeros(1, np.int64), rules, rm, snp.SeededRandom(seed)).chosen[0]
+        assert ch == mix64(seed, 0, 0) % 2
+        first += ch == 0
+    assert abs(first / 2000 - 0.5) <= 0.05
+
+
+def test_sv_calc_matches_oracle_with_random_state():
+    from oracle.snp_oracle import VectorEngine
+    rng = np.random.default_rng(5)
+    for i in range(0, 1000, 97):
+        osys = corpus_system(i)
+        a = to_system_arrays(osys)
+        ve = VectorEngine(osys, "compressed")
+        for trial in range(3):
+            cfg = rng.integers(0, 21, osys.q)
+            dly = rng.integers(0, 3, osys.q) * (rng.random(osys.q) < 0.3)
+            for pol, seed in ((0, 0), (1, 1234 + trial)):
+                sel = snp.FirstApplicable() if pol == 0 else snp.SeededRandom(seed)
+                got = snp.sv_calc(cfg, dly, a.rules, a.rule_map, sel, step=trial * 11).chosen
+                np.testing.assert_array_equal(got, ve.sv_calc(cfg, dly, pol, seed, trial * 11))
+
+
+def test_step_kernels_match_oracle_with_random_state():
+    from oracle.snp_oracle import VectorEngine
+    rng = np.random.default_rng(9)
+    for i in range(0, 1000, 89):
+        osys = corpus_system(i)
+        system = snp.gen_random(50, 4, 8, 20, 3, i)
+        rules, rm = snp.build_rule_vector(system)
+        mats = {"sparse": snp.build_sparse(system), "ell": snp.build_ell(system),
+                "compressed": snp.build_compressed(system)}
+        for trial in range(3):
+            cfg = rng.integers(0, 21, osys.q) + 40  # large enough to never go negative
+            dly = rng.integers(0, 3, osys.q) * (rng.random(osys.q) < 0.3)
+            chosen = VectorEngine(osys, "compressed").sv_calc(cfg, dly * 0, 0, 0, 0)
+            state = snp.SimState(cfg, dly, snp.SpikingVector(chosen))
+            for fmt, fn in (("sparse", snp.step_sparse), ("ell", snp.step_ell), ("compressed", snp.step_compressed)):
+                want = VectorEngine(osys, fmt).step(cfg, dly, chosen)
+                np.testing.assert_array_equal(fn(state, mats[fmt], rules), want)
+            want_d = VectorEngine(osys, "compressed").update_delays(dly, chosen)
+            np.testing.assert_array_equal(snp.update_delays(dly, snp.SpikingVector(chosen), rules), want_d)
+
+
+def test_step_single_rule_identity_and_closed_destination():
+    system = _relay()
+    rules, rm = snp.build_rule_vector(system)
+    mats = (snp.build_sparse(system), snp.build_ell(system), snp.build_compressed(system))
+    fns = (snp.step_sparse, snp.step_ell, snp.step_compressed)
+    cfg, z = np.array([2, 0]), np.zeros(2, dtype=np.int64)
+    sv = snp.sv_calc(cfg, z, rules, rm, snp.FirstApplicable())
+    for fn, mat in zip(fns, mats):
+        assert fn(snp.SimState(cfg, z, sv), mat, rules).tolist() == [0, 1]
+        empty = snp.SimState(np.array([1, 5]), z, snp.SpikingVector(np.full(2, -1, dtype=np.int64)))
+        assert fn(empty, mat, rules).tolist() == [1, 5]
+        closed = snp.SimState(np.array([2, 7]), np.array([0, 3]), sv)
+        assert fn(closed, mat, rules).tolist() == [0, 7]
+
+
+def test_ell_row_visits():
+    system = snp.gen_sort(snp.SortInstance(3))
+    rules, rm = snp.build_rule_vector(system)
+    cfg = np.zeros(9, dtype=np.int64)
+    cfg[3] = 2
+    z = np.zeros(9, dtype=np.int64)
+    sv = snp.sv_calc(cfg, z, rules, rm, snp.FirstApplicable())
+    visits = np.zeros(12, dtype=np.int64)
+    snp.step_ell(snp.SimState(cfg, z, sv), snp.build_ell(system), rules, row_visits=visits)
+    assert visits[int(sv.chosen[3])] == 2
+
+
+def test_update_delays_cases():
+    s = snp.SNPSystem()
+    a = s.add_neuron(1)
+    s.add_rule(a, snp.at_least(1), 1, 1, 3)
+    rules = snp.build_rule_vector(s.validate())[0]
+    none = snp.SpikingVector(np.full(3, -1, dtype=np.int64))
+    assert snp.update_delays(np.array([0, 2, 1]), none, rules).tolist() == [0, 1, 0]
+    assert snp.update_delays(np.zeros(1, np.int64), snp.SpikingVector(np.array([0])), rules).tolist() == [3]
+
+
+def test_negative_spikes_every_format():
+    s = snp.SNPSystem()
+    a = s.add_neuron(1)
+    s.add_rule(a, snp.at_least(1), 2, 1, 0)
+    s.validate()
+    for fmt, variant in FORMATS:
+        with pytest.raises(snp.NegativeSpikes):
+            snp.simulate(s, fmt, snp.SimOptions(max_steps=5)) if variant == "auto" else \
+                snp.simulate_prepared(snp.prepare(s, fmt, variant=variant), snp.SimOptions(max_steps=5))
+
+
+def test_loop_contract():
+    system = snp.gen_sort(snp.SortInstance(3))
+    tr = snp.simulate(system, snp.Format.SPARSE, snp.SimOptions(max_steps=1))
+    assert len(tr.configs) == 2 and tr.halt_reason is snp.HaltReason.STEP_LIMIT
+    s = snp.SNPSystem()
+    s.add_neuron(5)
+    s.validate()
+    tr = snp.simulate(s, snp.Format.COMPRESSED, snp.SimOptions(max_steps=10))
+    assert tr.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES and [c.tolist() for c in tr.configs] == [[5]]
+    empty = snp.SNPSystem().validate()
+    tr = snp.simulate(empty, snp.Format.SPARSE, snp.SimOptions(max_steps=3))
+    assert tr.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES and len(tr.configs) == 1
+    lean = snp.simulate(system, snp.Format.ELL, snp.SimOptions(max_steps=10))
+    assert lean.delays is None and lean.spiking is None
+    full = snp.simulate(system, snp.Format.ELL, snp.SimOptions(max_steps=10, record=snp.RecordLevel.FULL))
+    assert len(full.spiking) == full.steps and len(full.delays) == len(full.configs)
+    assert snp.format_trace(snp.simulate(_relay(), snp.Format.SPARSE, snp.SimOptions(max_steps=5))).splitlines()[0] == "2 0"
+
+
+def test_trace_chunking_is_invisible():
+    """Long recorded runs cross several device segments and host copies."""
+    a = snp.sort_arrays(snp.SortInstance(300))
+    prep = snp.prepare(a, snp.Format.COMPRESSED)
+    opts = snp.SimOptions(max_steps=400, record=snp.RecordLevel.FULL)
+    t1 = prep.engine.trace(opts, rows_per_call=7)
+    t2 = prep.engine.trace(opts)
+    assert t1 == t2 and t1.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
+    assert t1.configs[-1][600:].tolist() == list(range(1, 301))
