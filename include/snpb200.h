@@ -45,9 +45,10 @@ enum {
 /* matrices.py:33-45 Format (ORACLE has no device backend) */
 enum { SNP_FMT_SPARSE = 0, SNP_FMT_ELL = 1, SNP_FMT_COMPRESSED = 2 };
 
-/* COMPRESSED only: gather from in-adjacency (atomic-free, default) or the
- * paper's Alg. 5 push with atomics over the out-adjacency. */
-enum { SNP_VARIANT_AUTO = 0, SNP_VARIANT_PULL = 1, SNP_VARIANT_PUSH = 2 };
+/* COMPRESSED only: TILED (default) = destination tiles with source-sorted
+ * in-edge segments and shared-memory accumulation; PULL = per-destination
+ * CSR gather; PUSH = the paper's Alg. 5 scatter with atomics. */
+enum { SNP_VARIANT_AUTO = 0, SNP_VARIANT_PULL = 1, SNP_VARIANT_PUSH = 2, SNP_VARIANT_TILED = 3 };
 
 /* selection.py:21-31 */
 enum { SNP_POLICY_FIRST = 0, SNP_POLICY_SEEDED = 1 };
@@ -139,8 +140,10 @@ typedef struct snp_engine_info {
     int32_t format, variant;
     int32_t p_mode;           /* 0 bit (p common), 1 u8, 2 u16, 3 u32 */
     int32_t heavy_neurons;
-    int64_t in_edges;         /* pull: padded in-adjacency entries */
+    int64_t in_edges;         /* pull: padded in-adjacency entries; tiled: segment words */
     int64_t p_common;
+    int64_t tile;             /* tiled: destinations per tile */
+    int64_t n_tiles;
 } snp_engine_info;
 
 int snp_abi_version(void);

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 SNP_OK, SNP_ERR_NEGATIVE, SNP_ERR_BAD_ARG, SNP_ERR_CUDA, SNP_ERR_CAPACITY = range(5)
 SNP_FMT_SPARSE, SNP_FMT_ELL, SNP_FMT_COMPRESSED = range(3)
-SNP_VARIANT_AUTO, SNP_VARIANT_PULL, SNP_VARIANT_PUSH = range(3)
+SNP_VARIANT_AUTO, SNP_VARIANT_PULL, SNP_VARIANT_PUSH, SNP_VARIANT_TILED = range(4)
 SNP_REC_CONFIGS, SNP_REC_DELAYS, SNP_REC_SPIKING = 1, 2, 4
 SNP_RUNNING, SNP_HALT_STEP_LIMIT, SNP_HALT_NO_APPLICABLE, SNP_HALT_NEGATIVE = range(4)
 STAT_NAMES = ("steps", "scanned", "fired", "sending", "edges", "rows", "open")
@@ -75,6 +75,7 @@ class EngineInfo(ctypes.Structure):
         ("device_bytes", ctypes.c_int64), ("format", ctypes.c_int32), ("variant", ctypes.c_int32),
         ("p_mode", ctypes.c_int32), ("heavy_neurons", ctypes.c_int32),
         ("in_edges", ctypes.c_int64), ("p_common", ctypes.c_int64),
+        ("tile", ctypes.c_int64), ("n_tiles", ctypes.c_int64),
     ]
 
 

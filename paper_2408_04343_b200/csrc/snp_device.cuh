@@ -38,8 +38,21 @@ constexpr uint32_t kLightRules = 32;   // thread-per-neuron selection (32-bit ma
 constexpr uint32_t kLightIn = 256;     // thread-per-neuron gather
 constexpr uint32_t kLightOut = 64;     // thread-per-rule scatter
 constexpr uint32_t kExactBit = 0x80000000u;
+#ifndef SNP_STEP_MIN_BLOCKS
+#define SNP_STEP_MIN_BLOCKS 4
+#endif
+constexpr int kStepMinBlocks = SNP_STEP_MIN_BLOCKS;  // 4 caps the step kernel at 64 registers
+constexpr int kGatherBatch = 4;        // uint4 index loads in flight per gather round
 
 enum PMode { P_BIT = 0, P_U8 = 1, P_U16 = 2, P_U32 = 3 };
+
+// tiled pull layout
+constexpr int kTileThreads = 1024;
+constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
+constexpr uint32_t kDstBits = 15;         // destination slot within a tile
+constexpr uint32_t kSrcSpan = 1u << 17;   // source offset range within a segment
+constexpr uint32_t kDummyEdge = 0xffffffffu;
+constexpr int kMaxTile = (1 << kDstBits) - 32;
 enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
 enum Rec { REC_CONFIGS = 1, REC_DELAYS = 2, REC_SPIKING = 4 };
 enum Halt { RUNNING = 0, HALT_STEP_LIMIT = 1, HALT_NO_APPLICABLE = 2, HALT_NEGATIVE = 3 };
@@ -75,8 +88,9 @@ struct DevSys {
     long long q;
     long long m;
     const uint32_t* roff;     // [q+1] rule offsets
-    const uint32_t* rthr;     // [m] threshold | exact << 31
-    const int4* rrec;         // [m] {consumed, produced, delay, outdeg(owner)}
+    const void* rw;           // [m] rule words (compact uint2 / wide uint4), hot path
+    const int4* rrec;         // [m] {consumed, produced, delay, 0}, cold paths
+    const uint32_t* outdeg;   // [q] out-degree (traffic counters only)
     const uint32_t* ioff;     // pull: [q+1] in-adjacency offsets (4-aligned)
     const uint32_t* isrc;     // pull: sources, padded with the sentinel q
     const uint32_t* soff;     // push COMPRESSED: [q+1] out-adjacency
@@ -88,10 +102,19 @@ struct DevSys {
     long long dense_ld;
     const uint32_t* heavy;    // CTA-per-neuron list
     int n_heavy;
-    int light_blocks;
+    int light_ctas;           // CTAs striding over light tiles
+    int heavy_ctas;           // CTAs striding over the heavy list
+    long long light_tiles;    // ceil(q / 256)
     int z;                    // max out-degree
     int ell_rows;             // z + 1
     long long p_common;       // P_BIT: the single produced amount
+    // tiled pull (default COMPRESSED kernel)
+    const uint32_t* seg_words;  // [nseg * kSegEdges] (src - seg_base) << kDstBits | dst slot
+    const uint32_t* seg_base;   // [nseg] first source of each segment
+    const uint32_t* tseg;       // [n_tiles + 1] segment range of each tile
+    const uint32_t* theavy;     // [n_tiles + 1] range of s.heavy inside each tile
+    int tile;                   // destinations per tile (multiple of 32)
+    long long n_tiles;
 };
 
 struct DevState {
@@ -196,13 +219,13 @@ struct BlockStats {
 };
 
 // Block-wide reduction of per-thread stats into Ctrl (one atomic per counter).
-__device__ __forceinline__ void flush_stats(Ctrl* ctl, unsigned long long (&loc)[ST_COUNT]) {
+__device__ __forceinline__ void flush_stats(Ctrl* ctl, unsigned int (&loc)[ST_COUNT]) {
     __shared__ unsigned long long sh[ST_COUNT];
     if (threadIdx.x < ST_COUNT) sh[threadIdx.x] = 0;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < ST_COUNT; ++i) {
-        unsigned long long v = loc[i];
+        unsigned long long v = loc[i];  // per-thread counts fit 32 bits; sums may not
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sh[i], v);
@@ -254,15 +277,171 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
 }
 
 // ---------------------------------------------------------------------------
+// Rule words.  Compact: uint2 {guard, c | p << 16 | d << 24} when every rule
+// has c < 2^16, p < 2^8, d < 2^8 (one 8-byte word carries everything the
+// step needs, so selection and consumption read one sector per neuron);
+// otherwise wide: uint4 {guard, c, p, d}.
+template <bool WIDE>
+__device__ __forceinline__ uint4 load_rule(const void* __restrict__ rw, uint32_t r) {
+    if constexpr (WIDE) {
+        return __ldg(reinterpret_cast<const uint4*>(rw) + r);
+    } else {
+        const uint2 w = __ldg(reinterpret_cast<const uint2*>(rw) + r);
+        return make_uint4(w.x, w.y & 0xffffu, (w.y >> 16) & 0xffu, w.y >> 24);
+    }
+}
+template <bool WIDE>
+struct RuleRaw {
+    using T = uint2;
+};
+template <>
+struct RuleRaw<true> {
+    using T = uint4;
+};
+template <bool WIDE>
+__device__ __forceinline__ typename RuleRaw<WIDE>::T load_raw(const void* __restrict__ rw, uint32_t r) {
+    return __ldg(reinterpret_cast<const typename RuleRaw<WIDE>::T*>(rw) + r);
+}
+template <bool WIDE>
+__device__ __forceinline__ uint4 unpack_rule(typename RuleRaw<WIDE>::T w) {
+    if constexpr (WIDE) {
+        return w;
+    } else {
+        return make_uint4(w.x, w.y & 0xffffu, (w.y >> 16) & 0xffu, w.y >> 24);
+    }
+}
+__device__ __forceinline__ uint32_t rule_guard_word(const void* __restrict__ rw, bool wide, uint32_t r) {
+    return wide ? __ldg(reinterpret_cast<const uint4*>(rw) + r).x : __ldg(reinterpret_cast<const uint2*>(rw) + r).x;
+}
+
+// Gather over a 4-aligned, sentinel-padded in-list with batched independent
+// loads: kGatherBatch uint4 index loads in flight, then their P lookups.
+template <int PM>
+__device__ __forceinline__ long long gather_batched(const uint32_t* __restrict__ isrc,
+                                                    const uint32_t* __restrict__ P, uint32_t e0,
+                                                    uint32_t e1) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(isrc + e0);
+    const uint32_t n4 = (e1 - e0) >> 2;
+    long long acc = 0;
+    for (uint32_t b = 0; b < n4; b += kGatherBatch) {
+        uint4 v[kGatherBatch];
+#pragma unroll
+        for (int i = 0; i < kGatherBatch; ++i)
+            if (b + i < n4) v[i] = __ldg(p4 + b + i);
+#pragma unroll
+        for (int i = 0; i < kGatherBatch; ++i)
+            if (b + i < n4)
+                acc += p_lookup<PM>(P, v[i].x) + p_lookup<PM>(P, v[i].y) + p_lookup<PM>(P, v[i].z) +
+                       p_lookup<PM>(P, v[i].w);
+    }
+    return acc;
+}
+
+// Per-step constants shared by the step kernels.
+struct StepCtx {
+    long long k;
+    long long slot;
+    long long q;
+    unsigned long long seed;
+    uint32_t* Pcur;
+    int policy;
+    int record;
+    bool sel;
+    bool stats_on;
+};
+
+// Light-neuron tail of a step: C_k / D_k are final; records the trace rows,
+// applies the NegativeSpikes guard, selects among <= 32 rules (the first
+// four words w0..w3 were preloaded by the caller), commits Ĉ_k / delay state
+// / chosen and publishes non-bit P.  Returns the produced amount (0 if none).
+template <int KIND, int PM, bool CONSUME, bool FLIST, bool WIDE>
+__device__ __forceinline__ long long light_commit(const DevSys& s, const DevState& st, Ctrl* ctl, const StepCtx& cx,
+                                                  long long j, uint32_t r0, uint32_t nr,
+                                                  typename RuleRaw<WIDE>::T w0, typename RuleRaw<WIDE>::T w1,
+                                                  typename RuleRaw<WIDE>::T w2, typename RuleRaw<WIDE>::T w3,
+                                                  long long C, int D, bool can_sel, unsigned int (&stat)[ST_COUNT],
+                                                  bool& t_fired, bool& t_closed, bool& t_neg, long long& neg_idx,
+                                                  long long& neg_val, int& r) {
+    long long pval = 0;
+    if (C < 0) {
+        t_neg = true;
+        neg_idx = j;
+        neg_val = C;
+    }
+    if (cx.record & REC_CONFIGS) st.tr_cfg[cx.slot * cx.q + j] = C;
+    if (cx.record & REC_DELAYS) st.tr_dly[cx.slot * cx.q + j] = D;
+    t_closed |= D != 0;
+    uint4 wr = make_uint4(0, 0, 0, 0);
+    if (can_sel) {
+        uint32_t mask = (nr > 0 && guard_ok(w0.x, C) ? 1u : 0u) |
+                        (nr > 1 && guard_ok(w1.x, C) ? 2u : 0u) |
+                        (nr > 2 && guard_ok(w2.x, C) ? 4u : 0u) |
+                        (nr > 3 && guard_ok(w3.x, C) ? 8u : 0u);
+        for (uint32_t t = 4; t < nr; ++t)
+            mask |= (uint32_t)guard_ok(rule_guard_word(s.rw, WIDE, r0 + t), C) << t;
+        stat[ST_OPEN] += 1;
+        if (mask) {
+            int idx;
+            if (cx.policy == 0) {
+                idx = __ffs(mask) - 1;
+                stat[ST_SCANNED] += idx + 1;
+            } else {
+                idx = nth_set_bit(mask, (uint32_t)(mix64(cx.seed, cx.k, j) % (uint32_t)__popc(mask)));
+                stat[ST_SCANNED] += nr;
+            }
+            r = (int)(r0 + idx);
+            wr = unpack_rule<WIDE>(idx == 0 ? w0 : idx == 1 ? w1 : idx == 2 ? w2 : idx == 3 ? w3
+                                                                          : load_raw<WIDE>(s.rw, r));
+        } else {
+            stat[ST_SCANNED] += nr;
+        }
+    }
+    int nds = D;
+    long long Cn = C;
+    if (r >= 0) {
+        if (CONSUME) Cn -= (long long)wr.y;
+        pval = (long long)wr.z;
+        nds = -((int)wr.w + 1);
+        t_fired = true;
+        stat[ST_FIRED] += 1;
+        if (pval > 0) {
+            stat[ST_SENDING] += 1;
+            if (cx.stats_on) {
+                const uint32_t od = __ldg(s.outdeg + j);
+                stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
+            }
+        }
+        if (FLIST) {
+            unsigned int pos = atomicAdd(&ctl->list_count[cx.k & 1], 1u);
+            pick2(st.list, cx.k)[pos] = (uint32_t)r;
+        }
+    }
+    st.cfg[j] = Cn;
+    st.ds[j] = nds;
+    if (cx.sel) {
+        if (KIND == RECV_ARRAY) st.chosen[j] = r;
+        if (cx.record & REC_SPIKING) st.tr_chosen[cx.slot * cx.q + j] = r;
+        if (KIND == RECV_PULL && PM != P_BIT) {
+            if (PM == P_U8) reinterpret_cast<uint8_t*>(cx.Pcur)[j] = (uint8_t)pval;
+            else if (PM == P_U16) reinterpret_cast<uint16_t*>(cx.Pcur)[j] = (uint16_t)pval;
+            else cx.Pcur[j] = (uint32_t)pval;
+        }
+    }
+    return pval;
+}
+
+// ---------------------------------------------------------------------------
 // The fused step kernel.
 //
-// CTAs [0, light_blocks) map thread -> neuron j = blockIdx*256 + tid (light
-// neurons: <= 32 rules and, for pull, in-degree <= 256).  CTAs beyond that
-// each own one heavy neuron from s.heavy (e.g. the sorter's detectors with n
-// rules and n in-neighbours): block-strided gather + block-wide ballot scan.
+// Light CTAs (blockIdx < light_ctas) stride over 256-neuron tiles, thread ->
+// neuron (light neurons: <= 32 rules and, for pull, in-degree <= 256).  Heavy
+// CTAs stride over s.heavy, one neuron at a time (e.g. the sorter's detectors
+// with n rules and n in-neighbours): block-strided gather + block-wide ballot
+// scan.  The grid is sized to the resident capacity of the 148 SMs, so the
+// per-CTA end-of-step reductions are few.
 
-template <int KIND, int PM, bool CONSUME, bool FLIST>
-__global__ void __launch_bounds__(kBlock) step_kernel(DevSys s, DevState st) {
+template <int KIND, int PM, bool CONSUME, bool FLIST, bool WIDE>
+__global__ void __launch_bounds__(kBlock, kStepMinBlocks) step_kernel(DevSys s, DevState st) {
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     const int halted = vc->halted;
@@ -280,119 +459,80 @@ __global__ void __launch_bounds__(kBlock) step_kernel(DevSys s, DevState st) {
     const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
     uint32_t* Pcur = pick3(st.P, k % 3);
     uint32_t* Pzero = pick3(st.P, (k + 1) % 3);
-    const bool want_chosen = (KIND == RECV_ARRAY);
     const long long q = s.q;
+    const StepCtx cx{k, slot, q, seed, Pcur, policy, record, sel, stats_on};
 
-    unsigned long long stat[ST_COUNT];
+    unsigned int stat[ST_COUNT];
 #pragma unroll
     for (int i = 0; i < ST_COUNT; ++i) stat[i] = 0;
     bool t_fired = false, t_closed = false, t_neg = false;
     long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
 
-    if (blockIdx.x < (unsigned)s.light_blocks) {
+    if (blockIdx.x < (unsigned)s.light_ctas) {
         // ------------------------------------------------------------ light
-        const long long j = (long long)blockIdx.x * kBlock + threadIdx.x;
-        const bool active = j < q;
-        uint32_t r0 = 0, r1 = 0, e0 = 0, e1 = 0;
-        if (active) {
-            r0 = __ldg(s.roff + j);
-            r1 = __ldg(s.roff + j + 1);
-            if (KIND == RECV_PULL) {
-                e0 = __ldg(s.ioff + j);
-                e1 = __ldg(s.ioff + j + 1);
-            }
-        }
-        const bool heavy = active && ((r1 - r0) > kLightRules ||
-                                      (KIND == RECV_PULL && (e1 - e0) > kLightIn));
-        const bool mine = active && !heavy;
-        int r = -1;
-        long long pval = 0;
-        if (mine) {
-            long long C = st.cfg[j];
-            const int dsv = st.ds[j];
-            const bool open_prev = ds_open(dsv);
-            if (KIND == RECV_PULL) {
-                if (open_prev && e1 > e0) {
-                    long long g = gather_thread<PM>(s.isrc, Pprev, e0, e1);
-                    C += (PM == P_BIT) ? g * s.p_common : g;
-                    stat[ST_EDGES] += e1 - e0;
+        for (long long tile = blockIdx.x; tile < s.light_tiles; tile += s.light_ctas) {
+            const long long j = tile * kBlock + threadIdx.x;
+            const bool active = j < q;
+            uint32_t r0 = 0, r1 = 0, e0 = 0, e1 = 0;
+            long long Cprev = 0;
+            int dsv = 0;
+            if (active) {
+                r0 = __ldg(s.roff + j);
+                r1 = __ldg(s.roff + j + 1);
+                if (KIND == RECV_PULL) {
+                    e0 = __ldg(s.ioff + j);
+                    e1 = __ldg(s.ioff + j + 1);
                 }
-            } else {
-                const long long rv = st.recv[j];
-                if (rv != 0) st.recv[j] = 0;
-                if (open_prev) C += rv;
+                Cprev = st.cfg[j];
+                dsv = st.ds[j];
             }
-            const int D = ds_next(dsv);
-            if (C < 0) {
-                t_neg = true;
-                neg_idx = j;
-                neg_val = C;
-            }
-            if (record & REC_CONFIGS) st.tr_cfg[slot * q + j] = C;
-            if (record & REC_DELAYS) st.tr_dly[slot * q + j] = D;
-            t_closed = D != 0;
-            if (sel && D == 0) {
-                const uint32_t nr = r1 - r0;
-                uint32_t mask = 0;
-                for (uint32_t t = 0; t < nr; ++t) mask |= (uint32_t)guard_ok(__ldg(s.rthr + r0 + t), C) << t;
-                stat[ST_OPEN] += 1;
-                if (mask) {
-                    int idx;
-                    if (policy == 0) {
-                        idx = __ffs(mask) - 1;
-                        stat[ST_SCANNED] += idx + 1;
-                    } else {
-                        const uint32_t cnt = __popc(mask);
-                        idx = nth_set_bit(mask, (uint32_t)(mix64(seed, k, j) % cnt));
-                        stat[ST_SCANNED] += nr;
+            const uint32_t nr = r1 - r0;
+            const bool heavy = active && (nr > kLightRules || (KIND == RECV_PULL && (e1 - e0) > kLightIn));
+            const bool mine = active && !heavy;
+            int r = -1;
+            long long pval = 0;
+            if (mine) {
+                const bool open_prev = ds_open(dsv);
+                const int D = ds_next(dsv);
+                const bool can_sel = sel && D == 0;
+                // rule words of the first 4 rules, issued with the gather
+                using Raw = typename RuleRaw<WIDE>::T;
+                Raw w0{}, w1{}, w2{}, w3{};
+                if (can_sel) {
+                    if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                    if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                    if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                    if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                }
+                long long C = Cprev;
+                if (KIND == RECV_PULL) {
+                    if (open_prev && e1 > e0) {
+                        const long long g = gather_batched<PM>(s.isrc, Pprev, e0, e1);
+                        C += (PM == P_BIT) ? g * s.p_common : g;
+                        stat[ST_EDGES] += e1 - e0;
                     }
-                    r = (int)(r0 + idx);
                 } else {
-                    stat[ST_SCANNED] += nr;
+                    const long long rv = st.recv[j];
+                    if (rv != 0) st.recv[j] = 0;
+                    if (open_prev) C += rv;
                 }
+                pval = light_commit<KIND, PM, CONSUME, FLIST, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D,
+                                                                    can_sel, stat, t_fired, t_closed, t_neg, neg_idx,
+                                                                    neg_val, r);
             }
-            int nds = D;
-            long long Cn = C;
-            if (r >= 0) {
-                const int4 rec = __ldg(s.rrec + r);
-                if (CONSUME) Cn -= rec.x;
-                pval = rec.y;
-                nds = -(rec.z + 1);
-                t_fired = true;
-                stat[ST_FIRED] += 1;
-                if (pval > 0) {
-                    stat[ST_SENDING] += 1;
-                    stat[ST_ROWS] += (unsigned long long)rec.w + (rec.w < s.z ? 1 : 0);
-                }
-                if (FLIST) {
-                    unsigned int pos = atomicAdd(&ctl->list_count[k & 1], 1u);
-                    pick2(st.list, k)[pos] = (uint32_t)r;
-                }
-            }
-            st.cfg[j] = Cn;
-            st.ds[j] = nds;
-            if (sel) {
-                if (want_chosen) st.chosen[j] = r;
-                if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
-                if (KIND == RECV_PULL && PM != P_BIT) {
-                    if (PM == P_U8) reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)pval;
-                    else if (PM == P_U16) reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)pval;
-                    else Pcur[j] = (uint32_t)pval;
-                }
-            }
-        }
-        if (KIND == RECV_PULL && PM == P_BIT && sel) {
-            // one 32-neuron word per warp: lanes are consecutive neurons
-            const unsigned int bits = __ballot_sync(0xffffffffu, mine && pval > 0);
-            const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
-            const unsigned int act = __ballot_sync(0xffffffffu, active);
-            if ((threadIdx.x & 31) == 0 && act) {
-                const long long w = j >> 5;
-                Pzero[w] = 0u;
-                if (hv) {
-                    if (bits) atomicOr(Pcur + w, bits);
-                } else {
-                    Pcur[w] = bits;
+            if (KIND == RECV_PULL && PM == P_BIT && sel) {
+                // one 32-neuron word per warp: lanes are consecutive neurons
+                const unsigned int bits = __ballot_sync(0xffffffffu, mine && pval > 0);
+                const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
+                const unsigned int act = __ballot_sync(0xffffffffu, active);
+                if ((threadIdx.x & 31) == 0 && act) {
+                    const long long w = j >> 5;
+                    Pzero[w] = 0u;
+                    if (hv) {
+                        if (bits) atomicOr(Pcur + w, bits);
+                    } else {
+                        Pcur[w] = bits;
+                    }
                 }
             }
         }
@@ -401,130 +541,136 @@ __global__ void __launch_bounds__(kBlock) step_kernel(DevSys s, DevState st) {
         __shared__ long long sh_sum[kBlock / 32];
         __shared__ int sh_pick;
         __shared__ unsigned int sh_cnt[kBlock / 32];
-        const int h = blockIdx.x - s.light_blocks;
-        const long long j = s.heavy[h];
-        const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
-        long long C = st.cfg[j];
-        const int dsv = st.ds[j];
-        const bool open_prev = ds_open(dsv);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        if (KIND == RECV_PULL) {
-            long long part = 0;
-            if (open_prev) {
-                const uint32_t e0 = __ldg(s.ioff + j), e1 = __ldg(s.ioff + j + 1);
-                for (uint32_t e = e0 + threadIdx.x; e < e1; e += kBlock) part += p_lookup<PM>(Pprev, __ldg(s.isrc + e));
-                if (threadIdx.x == 0) stat[ST_EDGES] += e1 - e0;
-            }
-            part = warp_sum_ll(part);
-            if (lane == 0) sh_sum[wid] = part;
-            __syncthreads();
-            long long g = 0;
+        for (int h = blockIdx.x - s.light_ctas; h < s.n_heavy; h += s.heavy_ctas) {
+            const long long j = s.heavy[h];
+            const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
+            long long C = st.cfg[j];
+            const int dsv = st.ds[j];
+            const bool open_prev = ds_open(dsv);
+            __syncthreads();  // shared scratch reuse across iterations
+            if (KIND == RECV_PULL) {
+                long long part = 0;
+                if (open_prev) {
+                    const uint32_t e0 = __ldg(s.ioff + j), e1 = __ldg(s.ioff + j + 1);
+                    for (uint32_t e = e0 + threadIdx.x; e < e1; e += kBlock)
+                        part += p_lookup<PM>(Pprev, __ldg(s.isrc + e));
+                    if (threadIdx.x == 0) stat[ST_EDGES] += e1 - e0;
+                }
+                part = warp_sum_ll(part);
+                if (lane == 0) sh_sum[wid] = part;
+                __syncthreads();
+                long long g = 0;
 #pragma unroll
-            for (int w = 0; w < kBlock / 32; ++w) g += sh_sum[w];
-            C += (PM == P_BIT) ? g * s.p_common : g;
-        } else {
-            const long long rv = st.recv[j];
-            __syncthreads();
-            if (threadIdx.x == 0 && rv != 0) st.recv[j] = 0;
-            if (open_prev) C += rv;
-        }
-        const int D = ds_next(dsv);
-        if (threadIdx.x == 0) {
-            if (C < 0) {
-                t_neg = true;
-                neg_idx = j;
-                neg_val = C;
-            }
-            if (record & REC_CONFIGS) st.tr_cfg[slot * q + j] = C;
-            if (record & REC_DELAYS) st.tr_dly[slot * q + j] = D;
-            t_closed = D != 0;
-        }
-        int r = -1;
-        if (sel && D == 0) {
-            if (threadIdx.x == 0) {
-                sh_pick = -1;
-                stat[ST_OPEN] += 1;
-            }
-            __syncthreads();
-            if (policy == 0) {
-                for (uint32_t base = r0; base < r1; base += kBlock) {
-                    const uint32_t t = base + threadIdx.x;
-                    const bool ok = t < r1 && guard_ok(__ldg(s.rthr + t), C);
-                    if (__syncthreads_or(ok)) {
-                        const unsigned int b = __ballot_sync(0xffffffffu, ok);
-                        if (lane == 0 && b) atomicMin(reinterpret_cast<unsigned int*>(&sh_pick),
-                                                      base + wid * 32 + __ffs(b) - 1);
-                        __syncthreads();
-                        break;
-                    }
-                }
-                // sh_pick initialised to -1 == 0xffffffff (unsigned max)
-                r = sh_pick;
-                if (threadIdx.x == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
+                for (int w = 0; w < kBlock / 32; ++w) g += sh_sum[w];
+                C += (PM == P_BIT) ? g * s.p_common : g;
             } else {
-                uint32_t total = 0;
-                for (uint32_t base = r0; base < r1; base += kBlock) {
-                    const uint32_t t = base + threadIdx.x;
-                    total += __syncthreads_count(t < r1 && guard_ok(__ldg(s.rthr + t), C));
+                const long long rv = st.recv[j];
+                __syncthreads();
+                if (threadIdx.x == 0 && rv != 0) st.recv[j] = 0;
+                if (open_prev) C += rv;
+            }
+            const int D = ds_next(dsv);
+            if (threadIdx.x == 0) {
+                if (C < 0 && !t_neg) {
+                    t_neg = true;
+                    neg_idx = j;
+                    neg_val = C;
                 }
-                if (threadIdx.x == 0) stat[ST_SCANNED] += r1 - r0;
-                if (total) {
-                    uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
+                if (record & REC_CONFIGS) st.tr_cfg[slot * q + j] = C;
+                if (record & REC_DELAYS) st.tr_dly[slot * q + j] = D;
+                t_closed |= D != 0;
+            }
+            int r = -1;
+            if (sel && D == 0) {
+                if (threadIdx.x == 0) {
+                    sh_pick = -1;
+                    stat[ST_OPEN] += 1;
+                }
+                __syncthreads();
+                if (policy == 0) {
                     for (uint32_t base = r0; base < r1; base += kBlock) {
                         const uint32_t t = base + threadIdx.x;
-                        const bool ok = t < r1 && guard_ok(__ldg(s.rthr + t), C);
-                        const uint32_t c = __syncthreads_count(ok);
-                        if (want < c) {
+                        const bool ok = t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C);
+                        if (__syncthreads_or(ok)) {
                             const unsigned int b = __ballot_sync(0xffffffffu, ok);
-                            if (lane == 0) sh_cnt[wid] = __popc(b);
-                            __syncthreads();
-                            uint32_t before = 0;
-                            for (int w = 0; w < wid; ++w) before += sh_cnt[w];
-                            const uint32_t rank = before + __popc(b & ((1u << lane) - 1u));
-                            if (ok && rank == want) sh_pick = (int)t;
+                            if (lane == 0 && b)
+                                atomicMin(reinterpret_cast<unsigned int*>(&sh_pick), base + wid * 32 + __ffs(b) - 1);
                             __syncthreads();
                             break;
                         }
-                        want -= c;
                     }
+                    // sh_pick starts at -1 == 0xffffffff (unsigned max)
                     r = sh_pick;
+                    if (threadIdx.x == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
+                } else {
+                    uint32_t total = 0;
+                    for (uint32_t base = r0; base < r1; base += kBlock) {
+                        const uint32_t t = base + threadIdx.x;
+                        total += __syncthreads_count(t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
+                    }
+                    if (threadIdx.x == 0) stat[ST_SCANNED] += r1 - r0;
+                    if (total) {
+                        uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
+                        for (uint32_t base = r0; base < r1; base += kBlock) {
+                            const uint32_t t = base + threadIdx.x;
+                            const bool ok = t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C);
+                            const uint32_t c = __syncthreads_count(ok);
+                            if (want < c) {
+                                const unsigned int b = __ballot_sync(0xffffffffu, ok);
+                                if (lane == 0) sh_cnt[wid] = __popc(b);
+                                __syncthreads();
+                                uint32_t before = 0;
+                                for (int w = 0; w < wid; ++w) before += sh_cnt[w];
+                                const uint32_t rank = before + __popc(b & ((1u << lane) - 1u));
+                                if (ok && rank == want) sh_pick = (int)t;
+                                __syncthreads();
+                                break;
+                            }
+                            want -= c;
+                        }
+                        r = sh_pick;
+                    }
                 }
             }
-        }
-        if (threadIdx.x == 0) {
-            int nds = D;
-            long long Cn = C;
-            long long pval = 0;
-            if (r >= 0) {
-                const int4 rec = __ldg(s.rrec + r);
-                if (CONSUME) Cn -= rec.x;
-                pval = rec.y;
-                nds = -(rec.z + 1);
-                t_fired = true;
-                stat[ST_FIRED] += 1;
-                if (pval > 0) {
-                    stat[ST_SENDING] += 1;
-                    stat[ST_ROWS] += (unsigned long long)rec.w + (rec.w < s.z ? 1 : 0);
+            if (threadIdx.x == 0) {
+                int nds = D;
+                long long Cn = C;
+                long long pval = 0;
+                if (r >= 0) {
+                    const uint4 wr = load_rule<WIDE>(s.rw, r);
+                    if (CONSUME) Cn -= (long long)wr.y;
+                    pval = (long long)wr.z;
+                    nds = -((int)wr.w + 1);
+                    t_fired = true;
+                    stat[ST_FIRED] += 1;
+                    if (pval > 0) {
+                        stat[ST_SENDING] += 1;
+                        if (stats_on) {
+                            const uint32_t od = __ldg(s.outdeg + j);
+                            stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
+                        }
+                    }
+                    if (FLIST) {
+                        unsigned int pos = atomicAdd(&ctl->list_count[k & 1], 1u);
+                        pick2(st.list, k)[pos] = (uint32_t)r;
+                    }
                 }
-                if (FLIST) {
-                    unsigned int pos = atomicAdd(&ctl->list_count[k & 1], 1u);
-                    pick2(st.list, k)[pos] = (uint32_t)r;
-                }
-            }
-            st.cfg[j] = Cn;
-            st.ds[j] = nds;
-            if (sel) {
-                if (want_chosen) st.chosen[j] = r;
-                if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
-                if (KIND == RECV_PULL) {
-                    if (PM == P_BIT) {
-                        if (pval > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
-                    } else if (PM == P_U8) {
-                        reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)pval;
-                    } else if (PM == P_U16) {
-                        reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)pval;
-                    } else {
-                        Pcur[j] = (uint32_t)pval;
+                st.cfg[j] = Cn;
+                st.ds[j] = nds;
+                if (sel) {
+                    if (KIND == RECV_ARRAY) st.chosen[j] = r;
+                    if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
+                    if (KIND == RECV_PULL) {
+                        if (PM == P_BIT) {
+                            if (pval > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
+                        } else if (PM == P_U8) {
+                            reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)pval;
+                        } else if (PM == P_U16) {
+                            reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)pval;
+                        } else {
+                            Pcur[j] = (uint32_t)pval;
+                        }
                     }
                 }
             }
@@ -535,6 +681,220 @@ __global__ void __launch_bounds__(kBlock) step_kernel(DevSys s, DevState st) {
     const bool bf = __syncthreads_or(t_fired);
     const bool bc = __syncthreads_or(t_closed);
     // negative: smallest index within the block
+    __shared__ long long sh_neg_idx, sh_neg_val;
+    if (threadIdx.x == 0) sh_neg_idx = 0x7fffffffffffffffll;
+    __syncthreads();
+    if (t_neg) atomicMin(&sh_neg_idx, neg_idx);
+    __syncthreads();
+    if (t_neg && sh_neg_idx == neg_idx) sh_neg_val = neg_val;
+    const bool bn = __syncthreads_or(t_neg);
+    if (threadIdx.x == 0) finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Tiled pull step kernel (default for COMPRESSED).
+//
+// A CTA owns a tile of `s.tile` consecutive destinations.  Their in-edges are
+// stored sorted by source and cut into 256-edge segments whose sources span
+// < 2^17 (host build: build_tiles), each word = (src - seg_base) << 15 | slot.
+// Phase 1 streams the segments (2 x 128-bit loads per lane), looks the
+// sources up in P_{k-1} -- consecutive lookups fall in the same few 128-byte
+// lines, so they hit L1 -- and accumulates into per-destination counters in
+// shared memory.  Phase 2 finishes step k-1 and selects step k for every
+// destination (thread -> destination, coalesced).  Phase 3 selects for the
+// tile's heavy-rule neurons (> 32 rules), one warp each.
+template <int PM, bool WIDE>
+__global__ void __launch_bounds__(kTileThreads, 1) tiled_step_kernel(DevSys s, DevState st) {
+    extern __shared__ uint32_t acc[];  // [tile + 1]; slot `tile` absorbs nothing (dummy)
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    const int halted = vc->halted;
+    const long long k = vc->step;
+    if (halted || k >= vc->stop_at) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->push_armed = 0;
+        return;
+    }
+    const bool sel = k < vc->max_steps;
+    const int policy = vc->policy;
+    const unsigned long long seed = vc->seed;
+    const int record = vc->record;
+    const bool stats_on = vc->stats_on != 0;
+    const long long slot = k - vc->trace_base;
+    const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
+    uint32_t* Pcur = pick3(st.P, k % 3);
+    uint32_t* Pzero = pick3(st.P, (k + 1) % 3);
+    const long long q = s.q;
+    const StepCtx cx{k, slot, q, seed, Pcur, policy, record, sel, stats_on};
+    const int T = s.tile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kWarps = kTileThreads / 32;
+
+    unsigned int stat[ST_COUNT];
+#pragma unroll
+    for (int i = 0; i < ST_COUNT; ++i) stat[i] = 0;
+    bool t_fired = false, t_closed = false, t_neg = false;
+    long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
+
+    for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
+        const long long d0 = tile * T;
+        const int nd = (int)min((long long)T, q - d0);
+        for (int i = threadIdx.x; i <= T; i += kTileThreads) acc[i] = 0;
+        __syncthreads();
+
+        // ---- phase 1: receive sums
+        const uint32_t g0 = __ldg(s.tseg + tile), g1 = __ldg(s.tseg + tile + 1);
+        for (uint32_t g = g0 + warp; g < g1; g += kWarps) {
+            const uint32_t base = __ldg(s.seg_base + g);
+            const uint4* wp = reinterpret_cast<const uint4*>(s.seg_words + (size_t)g * kSegEdges) + lane * 2;
+            const uint4 a = __ldg(wp), b = __ldg(wp + 1);
+            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            uint32_t v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                v[e] = (w[e] != kDummyEdge) ? (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits)) : 0u;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (v[e]) atomicAdd(&acc[w[e] & ((1u << kDstBits) - 1u)], v[e]);
+                stat[ST_EDGES] += (w[e] != kDummyEdge) ? 1u : 0u;
+            }
+        }
+        __syncthreads();
+
+        // ---- phase 2: finish step k-1, select step k (light neurons)
+        const int nd32 = (nd + 31) & ~31;
+        for (int i = threadIdx.x; i < nd32; i += kTileThreads) {
+            const long long j = d0 + i;
+            const bool active = i < nd;
+            uint32_t r0 = 0, r1 = 0;
+            long long Cprev = 0;
+            int dsv = 0;
+            if (active) {
+                r0 = __ldg(s.roff + j);
+                r1 = __ldg(s.roff + j + 1);
+                Cprev = st.cfg[j];
+                dsv = st.ds[j];
+            }
+            const uint32_t nr = r1 - r0;
+            const bool heavy = active && nr > kLightRules;
+            int r = -1;
+            long long pval = 0;
+            if (active) {
+                const bool open_prev = ds_open(dsv);
+                const int D = ds_next(dsv);
+                const bool can_sel = sel && D == 0 && !heavy;
+                using Raw = typename RuleRaw<WIDE>::T;
+                Raw w0{}, w1{}, w2{}, w3{};
+                if (can_sel) {
+                    if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                    if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                    if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                    if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                }
+                long long C = Cprev;
+                if (open_prev) {
+                    const uint32_t g = acc[i];
+                    C += (PM == P_BIT) ? (long long)g * s.p_common : (long long)g;
+                }
+                // heavy-rule neurons commit C_k / D_k here (no selection);
+                // phase 3 selects and overwrites
+                pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D,
+                                                                    can_sel, stat, t_fired, t_closed, t_neg, neg_idx,
+                                                                    neg_val, r);
+            }
+            if (sel) {
+                if (PM == P_BIT) {
+                    const unsigned int bits = __ballot_sync(0xffffffffu, pval > 0);
+                    const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
+                    const unsigned int act = __ballot_sync(0xffffffffu, active);
+                    if (lane == 0 && act) {
+                        const long long wd = j >> 5;
+                        Pzero[wd] = 0u;
+                        if (hv) {
+                            if (bits) atomicOr(Pcur + wd, bits);
+                        } else {
+                            Pcur[wd] = bits;
+                        }
+                    }
+                }
+            }
+        }
+
+        // ---- phase 3: heavy-rule neurons of this tile, one warp each
+        const uint32_t h0 = __ldg(s.theavy + tile), h1 = __ldg(s.theavy + tile + 1);
+        if (sel && h1 > h0) {
+            __syncthreads();  // phase-2 commits of C_k / D_k are visible CTA-wide
+            for (uint32_t h = h0 + warp; h < h1; h += kWarps) {
+                const long long j = s.heavy[h];
+                const int D = st.ds[j];  // phase 2 stored D_k (>= 0, not fired)
+                if (D != 0) continue;
+                const long long C = st.cfg[j];
+                const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
+                int r = -1;
+                if (policy == 0) {
+                    for (uint32_t base = r0; base < r1 && r < 0; base += 32) {
+                        const uint32_t t = base + lane;
+                        const unsigned int b =
+                            __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
+                        if (b) r = (int)(base + __ffs(b) - 1);
+                    }
+                    if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
+                } else {
+                    uint32_t total = 0;
+                    for (uint32_t base = r0; base < r1; base += 32) {
+                        const uint32_t t = base + lane;
+                        total += __popc(__ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C)));
+                    }
+                    if (lane == 0) stat[ST_SCANNED] += r1 - r0;
+                    if (total) {
+                        uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
+                        for (uint32_t base = r0; base < r1; base += 32) {
+                            const uint32_t t = base + lane;
+                            const unsigned int b =
+                                __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
+                            const uint32_t c = __popc(b);
+                            if (want < c) {
+                                r = (int)(base + nth_set_bit(b, want));
+                                break;
+                            }
+                            want -= c;
+                        }
+                    }
+                }
+                if (lane == 0) {
+                    stat[ST_OPEN] += 1;
+                    if (r >= 0) {
+                        const uint4 wr = load_rule<WIDE>(s.rw, r);
+                        st.cfg[j] = C - (long long)wr.y;
+                        st.ds[j] = -((int)wr.w + 1);
+                        t_fired = true;
+                        stat[ST_FIRED] += 1;
+                        if (wr.z > 0) {
+                            stat[ST_SENDING] += 1;
+                            if (stats_on) {
+                                const uint32_t od = __ldg(s.outdeg + j);
+                                stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
+                            }
+                        }
+                        if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
+                        if (PM == P_BIT) {
+                            if (wr.z > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
+                        } else if (PM == P_U8) {
+                            reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)wr.z;
+                        } else if (PM == P_U16) {
+                            reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)wr.z;
+                        } else {
+                            Pcur[j] = wr.z;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // acc is reused by the next tile
+    }
+
+    if (stats_on) flush_stats(ctl, stat);
+    const bool bf = __syncthreads_or(t_fired);
+    const bool bc = __syncthreads_or(t_closed);
     __shared__ long long sh_neg_idx, sh_neg_val;
     if (threadIdx.x == 0) sh_neg_idx = 0x7fffffffffffffffll;
     __syncthreads();

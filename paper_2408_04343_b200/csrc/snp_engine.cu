@@ -55,8 +55,8 @@ using StepFn = void (*)(DevSys, DevState);
 using PrimeFn = void (*)(DevSys, DevState, const long long*, const long long*, const long long*);
 
 template <int KIND, int PM, bool CONSUME, bool FLIST>
-void pick_fns(StepFn* step, PrimeFn* prime) {
-    *step = step_kernel<KIND, PM, CONSUME, FLIST>;
+void pick_fns(bool wide, StepFn* step, PrimeFn* prime) {
+    *step = wide ? step_kernel<KIND, PM, CONSUME, FLIST, true> : step_kernel<KIND, PM, CONSUME, FLIST, false>;
     *prime = prime_kernel<KIND, PM, CONSUME, FLIST>;
 }
 
@@ -72,6 +72,11 @@ struct snp_engine {
     long long p_common = 1;
     long long in_edges = 0;
     int kind = RECV_PULL;
+    bool tiled = false;
+    int step_block = kBlock;
+    size_t step_smem = 0;
+    bool wide_rules = false;
+    long long resident_ctas = 0;
     cudaStream_t stream = nullptr;
     std::vector<void*> allocs;
     long long device_bytes = 0;
@@ -140,6 +145,80 @@ int grid_for(long long n, int block = 256) {
     return (int)std::max<long long>(1, std::min<long long>(ceil_div(n, block), 1ll << 30));
 }
 
+// Tiled-pull layout (see tiled_step_kernel): destinations are cut into
+// tiles of T; each tile's in-edges, visited in ascending source order (the
+// CSR out-adjacency is source-major, so a stable bucket pass keeps that
+// order), are packed into 256-edge segments whose sources span < 2^17.
+int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff,
+                const std::vector<uint32_t>& sdst, std::vector<uint32_t>& heavy) {
+    const long long q = e->q;
+    DevSys& s = e->sys;
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, e->device);
+    // heavy-rule neurons only (in-degree does not matter here)
+    heavy.clear();
+    for (long long i = 0; i < q; ++i)
+        if (d->offsets[i + 1] - d->offsets[i] > (long long)kLightRules) heavy.push_back((uint32_t)i);
+    long long T = ceil_div(std::max<long long>(q, 1), 4ll * n_sm);
+    if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
+    if (const char* env = getenv("SNPB200_TILE")) T = atoll(env);
+    T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
+    const long long n_tiles = std::max<long long>(1, ceil_div(q, T));
+    s.tile = (int)T;
+    s.n_tiles = n_tiles;
+    // bucket the edges by destination tile (source order preserved)
+    const long long S = (long long)sdst.size();
+    std::vector<unsigned long long> start(n_tiles + 1, 0);
+    for (long long e2 = 0; e2 < S; ++e2) start[sdst[e2] / T + 1]++;
+    for (long long t = 0; t < n_tiles; ++t) start[t + 1] += start[t];
+    std::vector<unsigned long long> cur(start.begin(), start.end() - 1);
+    std::vector<uint32_t> bsrc(S);
+    std::vector<uint16_t> bslot(S);
+    for (long long i = 0; i < q; ++i)
+        for (uint32_t e2 = soff[i]; e2 < soff[i + 1]; ++e2) {
+            const uint32_t dst = sdst[e2];
+            const unsigned long long pos = cur[dst / T]++;
+            bsrc[pos] = (uint32_t)i;
+            bslot[pos] = (uint16_t)(dst % T);
+        }
+    // segments
+    std::vector<uint32_t> tseg(n_tiles + 1, 0), base;
+    std::vector<uint32_t> words;
+    words.reserve((size_t)(S + S / 8 + 256));
+    for (long long t = 0; t < n_tiles; ++t) {
+        unsigned long long e2 = start[t];
+        const unsigned long long end = start[t + 1];
+        while (e2 < end) {
+            const uint32_t b = bsrc[e2];
+            base.push_back(b);
+            int n = 0;
+            while (e2 < end && n < kSegEdges && bsrc[e2] - b < kSrcSpan) {
+                words.push_back(((bsrc[e2] - b) << kDstBits) | bslot[e2]);
+                ++e2;
+                ++n;
+            }
+            for (; n < kSegEdges; ++n) words.push_back(kDummyEdge);
+        }
+        tseg[t + 1] = (uint32_t)base.size();
+        if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
+    }
+    // heavy-rule neurons per tile (heavy is ascending)
+    std::vector<uint32_t> theavy(n_tiles + 1, 0);
+    for (uint32_t hn : heavy) theavy[hn / T + 1]++;
+    for (long long t = 0; t < n_tiles; ++t) theavy[t + 1] += theavy[t];
+    uint32_t *d_words, *d_base, *d_tseg, *d_theavy;
+    TRY(upload(e, &d_words, words));
+    TRY(upload(e, &d_base, base));
+    TRY(upload(e, &d_tseg, tseg));
+    TRY(upload(e, &d_theavy, theavy));
+    s.seg_words = d_words;
+    s.seg_base = d_base;
+    s.tseg = d_tseg;
+    s.theavy = d_theavy;
+    e->in_edges = (long long)words.size();
+    return SNP_OK;
+}
+
 // Build every device structure.  Host-side work is O(q + m + S) with plain
 // loops; the quadratic layouts (ELL pairs, dense rows) and the in-adjacency
 // transpose are built on the device.
@@ -170,6 +249,7 @@ int build(snp_engine* e, const snp_system_desc* d) {
     if ((q > 0 ? d->offsets[q] : 0) != m) return fail(SNP_ERR_BAD_ARG, "offsets[q] != m");
     std::vector<uint32_t> rthr(m);
     std::vector<int4> rrec(m);
+    bool compact = true;
     long long pmax = 0, pfirst = -1;
     bool pcommon = true;
     for (long long r = 0; r < m; ++r) {
@@ -180,6 +260,7 @@ int build(snp_engine* e, const snp_system_desc* d) {
         if (dl < 0 || dl > kInt32Max - 2) return fail(SNP_ERR_CAPACITY, "rule %lld delay %lld outside [0, 2^31-3]", r, dl);
         rthr[r] = (uint32_t)t | (d->is_exact[r] ? kExactBit : 0u);
         rrec[r] = make_int4((int)c, (int)p, (int)dl, 0);
+        if (c >= 65536 || p >= 256 || dl >= 256) compact = false;
         if (p > 0) {
             pmax = std::max(pmax, p);
             if (pfirst < 0) pfirst = p;
@@ -220,10 +301,12 @@ int build(snp_engine* e, const snp_system_desc* d) {
         have_adj = true;
     }
     int z = 0;
+    std::vector<uint32_t> outdeg(q, 0);
     if (have_adj)
-        for (long long i = 0; i < q; ++i) z = std::max<int>(z, (int)(soff[i + 1] - soff[i]));
-    if (have_adj)
-        for (long long r = 0; r < m; ++r) rrec[r].w = (int)(soff[owner[r] + 1] - soff[owner[r]]);
+        for (long long i = 0; i < q; ++i) {
+            outdeg[i] = soff[i + 1] - soff[i];
+            z = std::max<int>(z, (int)outdeg[i]);
+        }
 
     const bool ell_from_matrix = e->format == SNP_FMT_ELL && !have_adj;
     const bool dense_from_matrix = e->format == SNP_FMT_SPARSE && !have_adj;
@@ -253,7 +336,7 @@ int build(snp_engine* e, const snp_system_desc* d) {
                 ++n;
             }
             ell_len_host[r] = (uint32_t)n;
-            rrec[r].w = (int)std::max<long long>(0, n - 1);
+            outdeg[owner[r]] = std::max<uint32_t>(outdeg[owner[r]], (uint32_t)std::max<long long>(0, n - 1));
         }
     }
     e->z = z;
@@ -261,8 +344,9 @@ int build(snp_engine* e, const snp_system_desc* d) {
     // --- receive path and P width
     e->variant = d->variant;
     if (e->format == SNP_FMT_COMPRESSED) {
-        if (e->variant == SNP_VARIANT_AUTO) e->variant = SNP_VARIANT_PULL;
+        if (e->variant == SNP_VARIANT_AUTO) e->variant = SNP_VARIANT_TILED;
         e->kind = e->variant == SNP_VARIANT_PUSH ? RECV_ARRAY : RECV_PULL;
+        e->tiled = e->variant == SNP_VARIANT_TILED;
     } else {
         e->variant = SNP_VARIANT_PUSH;
         e->kind = RECV_ARRAY;
@@ -291,14 +375,30 @@ int build(snp_engine* e, const snp_system_desc* d) {
     s.ell_rows = z + 1;
     s.p_common = e->p_common;
     uint32_t* d_roff;
-    uint32_t* d_rthr;
     int4* d_rrec;
+    uint32_t* d_outdeg;
     TRY(upload(e, &d_roff, roff));
-    TRY(upload(e, &d_rthr, rthr));
     TRY(upload(e, &d_rrec, rrec));
+    TRY(upload(e, &d_outdeg, outdeg));
     s.roff = d_roff;
-    s.rthr = d_rthr;
     s.rrec = d_rrec;
+    s.outdeg = d_outdeg;
+    e->wide_rules = !compact;
+    if (compact) {
+        std::vector<uint2> rw(m);
+        for (long long r = 0; r < m; ++r)
+            rw[r] = make_uint2(rthr[r], (uint32_t)rrec[r].x | ((uint32_t)rrec[r].y << 16) | ((uint32_t)rrec[r].z << 24));
+        uint2* d_rw;
+        TRY(upload(e, &d_rw, rw));
+        s.rw = d_rw;
+    } else {
+        std::vector<uint4> rw(m);
+        for (long long r = 0; r < m; ++r)
+            rw[r] = make_uint4(rthr[r], (uint32_t)rrec[r].x, (uint32_t)rrec[r].y, (uint32_t)rrec[r].z);
+        uint4* d_rw;
+        TRY(upload(e, &d_rw, rw));
+        s.rw = d_rw;
+    }
 
     uint32_t *d_soff = nullptr, *d_sdst = nullptr, *d_owner = nullptr;
     const bool need_owner = (e->format != SNP_FMT_COMPRESSED && have_adj);
@@ -310,7 +410,7 @@ int build(snp_engine* e, const snp_system_desc* d) {
 
     // heavy list (CTA per neuron)
     std::vector<uint32_t> indeg;
-    if (e->kind == RECV_PULL && q > 0) {
+    if (e->kind == RECV_PULL && !e->tiled && q > 0) {
         // in-adjacency = transpose of the out-adjacency, lists padded to x4
         // with the sentinel source q (whose P entry is always 0)
         uint32_t* d_indeg;
@@ -347,17 +447,17 @@ int build(snp_engine* e, const snp_system_desc* d) {
     std::vector<uint32_t> heavy;
     for (long long i = 0; i < q; ++i) {
         const bool many_rules = roff[i + 1] - roff[i] > kLightRules;
-        const bool many_in = e->kind == RECV_PULL && ((indeg[i] + 3u) & ~3u) > kLightIn;
+        const bool many_in = e->kind == RECV_PULL && !e->tiled && ((indeg[i] + 3u) & ~3u) > kLightIn;
         if (many_rules || many_in) heavy.push_back((uint32_t)i);
     }
+    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, heavy));
     uint32_t* d_heavy;
     TRY(upload(e, &d_heavy, heavy));
     s.heavy = d_heavy;
     s.n_heavy = (int)heavy.size();
-    // at least one (possibly all-idle) light CTA so that q == 0 still runs
+    // at least one (possibly all-idle) light tile so that q == 0 still runs
     // the halting decision on the device
-    s.light_blocks = (int)std::max<long long>(1, ceil_div(q, kBlock));
-    e->step_grid = s.light_blocks + s.n_heavy;
+    s.light_tiles = std::max<long long>(1, ceil_div(q, kBlock));
 
     if (e->format == SNP_FMT_COMPRESSED && e->kind == RECV_ARRAY) {
         s.soff = d_soff;
@@ -431,19 +531,49 @@ int build(snp_engine* e, const snp_system_desc* d) {
     e->heavy_push_grid = 148 * 4;
 
     // kernel instances
-    if (e->format == SNP_FMT_COMPRESSED && e->kind == RECV_PULL) {
+    if (e->tiled) {
+        auto pick = [&](auto wide_k, auto narrow_k, PrimeFn prime) {
+            e->step_fn = e->wide_rules ? wide_k : narrow_k;
+            e->prime_fn = prime;
+        };
         switch (e->p_mode) {
-            case P_BIT: pick_fns<RECV_PULL, P_BIT, true, false>(&e->step_fn, &e->prime_fn); break;
-            case P_U8: pick_fns<RECV_PULL, P_U8, true, false>(&e->step_fn, &e->prime_fn); break;
-            case P_U16: pick_fns<RECV_PULL, P_U16, true, false>(&e->step_fn, &e->prime_fn); break;
-            default: pick_fns<RECV_PULL, P_U32, true, false>(&e->step_fn, &e->prime_fn); break;
+            case P_BIT: pick(tiled_step_kernel<P_BIT, true>, tiled_step_kernel<P_BIT, false>, prime_kernel<RECV_PULL, P_BIT, true, false>); break;
+            case P_U8: pick(tiled_step_kernel<P_U8, true>, tiled_step_kernel<P_U8, false>, prime_kernel<RECV_PULL, P_U8, true, false>); break;
+            case P_U16: pick(tiled_step_kernel<P_U16, true>, tiled_step_kernel<P_U16, false>, prime_kernel<RECV_PULL, P_U16, true, false>); break;
+            default: pick(tiled_step_kernel<P_U32, true>, tiled_step_kernel<P_U32, false>, prime_kernel<RECV_PULL, P_U32, true, false>); break;
+        }
+    } else if (e->format == SNP_FMT_COMPRESSED && e->kind == RECV_PULL) {
+        switch (e->p_mode) {
+            case P_BIT: pick_fns<RECV_PULL, P_BIT, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn); break;
+            case P_U8: pick_fns<RECV_PULL, P_U8, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn); break;
+            case P_U16: pick_fns<RECV_PULL, P_U16, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn); break;
+            default: pick_fns<RECV_PULL, P_U32, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn); break;
         }
     } else if (e->format == SNP_FMT_COMPRESSED) {
-        pick_fns<RECV_ARRAY, P_BIT, true, false>(&e->step_fn, &e->prime_fn);
+        pick_fns<RECV_ARRAY, P_BIT, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn);
     } else if (e->format == SNP_FMT_ELL) {
-        pick_fns<RECV_ARRAY, P_BIT, false, false>(&e->step_fn, &e->prime_fn);
+        pick_fns<RECV_ARRAY, P_BIT, false, false>(e->wide_rules, &e->step_fn, &e->prime_fn);
     } else {
-        pick_fns<RECV_ARRAY, P_BIT, false, true>(&e->step_fn, &e->prime_fn);
+        pick_fns<RECV_ARRAY, P_BIT, false, true>(e->wide_rules, &e->step_fn, &e->prime_fn);
+    }
+    // persistent-style grid: as many CTAs as are resident at once
+    int per_sm = 0, n_sm = 0;
+    CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, e->device));
+    if (e->tiled) {
+        e->step_block = kTileThreads;
+        e->step_smem = (size_t)(s.tile + 1) * sizeof(uint32_t);
+        CU(cudaFuncSetAttribute(e->step_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, kTileThreads, e->step_smem));
+        const long long resident = (long long)std::max(1, per_sm) * std::max(1, n_sm);
+        e->step_grid = (int)std::min<long long>(s.n_tiles, resident);
+        e->resident_ctas = resident;
+    } else {
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, kBlock, 0));
+        const long long resident = (long long)std::max(1, per_sm) * std::max(1, n_sm);
+        s.light_ctas = (int)std::min<long long>(s.light_tiles, resident);
+        s.heavy_ctas = (int)std::min<long long>(s.n_heavy, resident);
+        e->step_grid = s.light_ctas + s.heavy_ctas;
+        e->resident_ctas = resident;
     }
     CU(cudaDeviceSynchronize());
     return SNP_OK;
@@ -452,7 +582,7 @@ int build(snp_engine* e, const snp_system_desc* d) {
 // Launch one step's kernels on the engine stream; returns launch count.
 int launch_step(snp_engine* e, long long* row_visits = nullptr) {
     int n = 1;
-    e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+    e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
     if (e->kind == RECV_ARRAY) {
         if (e->format == SNP_FMT_SPARSE) {
             dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
@@ -621,6 +751,8 @@ int snp_engine_get_info(const snp_engine* e, snp_engine_info* info) {
     info->heavy_neurons = e->sys.n_heavy;
     info->in_edges = e->in_edges;
     info->p_common = e->p_common;
+    info->tile = e->sys.tile;
+    info->n_tiles = e->sys.n_tiles;
     return SNP_OK;
 }
 
@@ -770,7 +902,7 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
         CU(cudaEventRecord(e->ev0, e->stream));
         for (long long i = 0; i < steps; ++i) {
             CU(cudaEventRecord(ev[2 * i], e->stream));
-            e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+            e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
             CU(cudaEventRecord(ev[2 * i + 1], e->stream));
             launches += 1;
             if (e->kind == RECV_ARRAY) {
@@ -858,7 +990,7 @@ int snp_sv_calc(snp_engine* e, const int64_t* config, const int64_t* delays, int
     c.seed = seed;
     c.record = REC_SPIKING;
     TRY(push_ctrl(e));
-    e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+    e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
     CU(cudaGetLastError());
     if (q > 0) {
         widen_i32_kernel<<<grid_for(q), 256, 0, e->stream>>>(q, e->st.tr_chosen, e->scratch[2]);
@@ -914,7 +1046,7 @@ int snp_step(snp_engine* e, const int64_t* config, const int64_t* delays, const 
         }
         CU(cudaGetLastError());
     }
-    e->step_fn<<<e->step_grid, kBlock, 0, e->stream>>>(e->sys, e->st);  // finalize only
+    e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);  // finalize only
     CU(cudaGetLastError());
     TRY(pull_ctrl(e));
     e->begun = false;

@@ -22,7 +22,8 @@ not depend on it (as in the reference, engine.py:15-17).
 Differences (documented in INTEGRATION.md): ``Format.ORACLE`` is the
 reference's CPU interpreter; it is test infrastructure here (``oracle/``),
 so ``prepare(..., Format.ORACLE)`` raises ``ValueError``.  Extensions:
-``variant`` on ``prepare`` (COMPRESSED pull vs the paper's push), and
+``variant`` on ``prepare`` (COMPRESSED: "tiled" (default), "pull", or the
+paper's "push"), and
 ``run_final`` (final state + traffic counters, no per-step trace).
 """
 
@@ -78,7 +79,8 @@ _REC_FLAGS = {
 }
 _FMT_CODES = {Format.SPARSE: nat.SNP_FMT_SPARSE, Format.ELL: nat.SNP_FMT_ELL,
               Format.COMPRESSED: nat.SNP_FMT_COMPRESSED}
-_VARIANTS = {"auto": nat.SNP_VARIANT_AUTO, "pull": nat.SNP_VARIANT_PULL, "push": nat.SNP_VARIANT_PUSH}
+_VARIANTS = {"auto": nat.SNP_VARIANT_AUTO, "pull": nat.SNP_VARIANT_PULL, "push": nat.SNP_VARIANT_PUSH,
+             "tiled": nat.SNP_VARIANT_TILED}
 
 
 @dataclass(frozen=True)

@@ -16,9 +16,9 @@ from oracle.snp_oracle import OracleSystem, trace_digest
 
 pytestmark = pytest.mark.gpu
 
-FORMATS = [(snp.Format.SPARSE, "auto"), (snp.Format.ELL, "auto"), (snp.Format.COMPRESSED, "pull"),
-           (snp.Format.COMPRESSED, "push")]
-FMT_IDS = ["sparse", "ell", "compressed-pull", "compressed-push"]
+FORMATS = [(snp.Format.SPARSE, "auto"), (snp.Format.ELL, "auto"), (snp.Format.COMPRESSED, "tiled"),
+           (snp.Format.COMPRESSED, "pull"), (snp.Format.COMPRESSED, "push")]
+FMT_IDS = ["sparse", "ell", "compressed-tiled", "compressed-pull", "compressed-push"]
 POLICIES = {"first": snp.FirstApplicable(), "seeded7": snp.SeededRandom(7),
             "seeded_big": snp.SeededRandom(2**63 + 5)}
 
@@ -52,7 +52,7 @@ def test_corpus_matches_reference_digests(fmt, variant):
     L=100, FULL traces identical to the reference (sha256 of every row)."""
     c = golden_npz("corpus.npz")
     L = int(c["L"])
-    n = corpus_size() if (fmt is snp.Format.COMPRESSED and variant == "pull") else 400
+    n = corpus_size() if (fmt is snp.Format.COMPRESSED and variant == "tiled") else 400
     for i in range(n):
         prep = snp.prepare(to_system_arrays(corpus_system(i)), fmt, variant=variant)
         for sel, key in ((snp.FirstApplicable(), "first"), (snp.SeededRandom(i), "seeded")):
@@ -97,7 +97,8 @@ def test_sorting_end_to_end(fmt, variant, n):
         assert trace_digest(tr.configs) == str(t["sort100/digest"])
 
 
-@pytest.mark.parametrize("n,fmts", [(512, FORMATS), (2048, [(snp.Format.COMPRESSED, "pull"),
+@pytest.mark.parametrize("n,fmts", [(512, FORMATS), (2048, [(snp.Format.COMPRESSED, "tiled"),
+                                                            (snp.Format.COMPRESSED, "pull"),
                                                             (snp.Format.COMPRESSED, "push")])])
 def test_sort_large_halts_sorted(n, fmts):
     """Heavy-neuron path (detectors own n rules and n in-neighbours)."""
@@ -150,12 +151,13 @@ def test_full_size_formats_agree():
     """ELL and push-Optimized reach the same state as pull-Optimized at 10^7."""
     a = snp.synth_v1(10_000_000, with_delays=True)
     finals = []
-    for fmt, variant in [(snp.Format.COMPRESSED, "pull"), (snp.Format.COMPRESSED, "push"), (snp.Format.ELL, "auto")]:
+    for fmt, variant in [(snp.Format.COMPRESSED, "tiled"), (snp.Format.COMPRESSED, "pull"),
+                         (snp.Format.COMPRESSED, "push"), (snp.Format.ELL, "auto")]:
         prep = snp.prepare(a, fmt, variant=variant)
         finals.append(snp.run_final(prep, snp.SimOptions(max_steps=4)).config)
         del prep
-    np.testing.assert_array_equal(finals[0], finals[1])
-    np.testing.assert_array_equal(finals[0], finals[2])
+    for other in finals[1:]:
+        np.testing.assert_array_equal(finals[0], other)
 
 
 # -- phase functions (test_engine.py:66-259) --------------------------------------------------
