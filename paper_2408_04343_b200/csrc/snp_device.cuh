@@ -47,7 +47,11 @@ constexpr int kGatherBatch = 4;        // uint4 index loads in flight per gather
 enum PMode { P_BIT = 0, P_U8 = 1, P_U16 = 2, P_U32 = 3 };
 
 // tiled pull layout
-constexpr int kTileThreads = 1024;
+#ifndef SNP_TILE_THREADS
+#define SNP_TILE_THREADS 992  // 31 consumer warps + 1 producer warp = 1024 threads
+#endif
+constexpr int kTileThreads = SNP_TILE_THREADS;  // consumer threads per CTA (multiple of 32)
+static_assert(kTileThreads % 32 == 0 && kTileThreads + 32 <= 1024, "CTA must fit 1024 threads");
 constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
 constexpr uint32_t kDstBits = 15;         // destination slot within a tile
 constexpr uint32_t kSrcSpan = 1u << 17;   // source offset range within a segment
@@ -84,6 +88,8 @@ struct Ctrl {
     unsigned int heavy_count[2];  // push heavy queue, by step parity
 };
 
+struct StageDesc;
+
 struct DevSys {
     long long q;
     long long m;
@@ -111,6 +117,9 @@ struct DevSys {
     // tiled pull (default COMPRESSED kernel)
     const uint32_t* seg_words;  // [nseg * kSegEdges] (src - seg_base) << kDstBits | dst slot
     const uint32_t* seg_base;   // [nseg] first source of each segment
+    const StageDesc* stages;    // TMA stage descriptors, tile-major (build_tiles)
+    const uint32_t* tstage;     // [n_tiles + 1] stage range of each tile
+    const uint32_t* stage_bases;  // segment bases per phase-1 stage (16-byte aligned runs)
     const uint32_t* tseg;       // [n_tiles + 1] segment range of each tile
     const uint32_t* theavy;     // [n_tiles + 1] range of s.heavy inside each tile
     int tile;                   // destinations per tile (multiple of 32)
@@ -692,20 +701,114 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) step_kernel(DevSys s, 
 }
 
 // ---------------------------------------------------------------------------
+// TMA bulk-copy pipeline helpers (cp.async.bulk + mbarrier, sm_90+/sm_100a).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier over the consumer warps only (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Tiled pull step kernel (default for COMPRESSED).
 //
 // A CTA owns a tile of `s.tile` consecutive destinations.  Their in-edges are
 // stored sorted by source and cut into 256-edge segments whose sources span
 // < 2^17 (host build: build_tiles), each word = (src - seg_base) << 15 | slot.
-// Phase 1 streams the segments (2 x 128-bit loads per lane), looks the
-// sources up in P_{k-1} -- consecutive lookups fall in the same few 128-byte
-// lines, so they hit L1 -- and accumulates into per-destination counters in
-// shared memory.  Phase 2 finishes step k-1 and selects step k for every
-// destination (thread -> destination, coalesced).  Phase 3 selects for the
-// tile's heavy-rule neurons (> 32 rules), one warp each.
+// Warp-specialised: one producer warp streams everything the tile needs from
+// HBM through a kRingStages-deep TMA ring in shared memory (cp.async.bulk,
+// full/empty mbarriers); the consumer warps never wait on each other except
+// at the two phase boundaries of a tile:
+//   phase 1 stages: 16 segments (16 KB); each warp takes one segment, looks
+//     its sources up in P_{k-1} (consecutive lookups hit the same L1 lines)
+//     and accumulates into per-destination counters in shared memory;
+//   phase 2 stages: 1024 destinations' Ĉ, delay state and rule offsets;
+//     each thread finishes step k-1 and selects step k for two destinations.
+// Phase 3 selects for the tile's heavy-rule neurons (> 32 rules), one warp
+// each.  The ring spans tiles, so the next tile's first segments are already
+// in flight while phase 3 / phase 2 finish.
+
+#ifndef SNP_RING_STAGES
+#define SNP_RING_STAGES 2
+#endif
+constexpr int kRingStages = SNP_RING_STAGES;
+constexpr int kWarpsC = kTileThreads / 32;              // consumer warps
+constexpr uint32_t kStageBytes = 64u * 1024u;           // one ring stage
+constexpr uint32_t kHdrBytes = 512;                     // stage header (+ segment bases)
+constexpr uint32_t kMaxSegPerStage = (kHdrBytes - 32) / 4;
+constexpr int kSub = kTileThreads;                      // destinations per phase-2 stage
+
+// Stage header, written by the producer thread with st.shared before the
+// mbarrier arrive (release), read by consumers after the wait (acquire).
+struct StageHdr {
+    uint32_t kind;     // 1 = phase-1 (segments), 2 = phase-2 (destinations)
+    uint32_t last;     // last stage of its phase for this tile
+    uint32_t first;    // phase 1: first segment; phase 2: first destination (tile index)
+    uint32_t n;        // segments / destinations in the stage
+    uint32_t src0;     // phase 1: first source bit of the staged P window (multiple of 128)
+    uint32_t pstaged;  // phase 1: P window staged in smem
+    uint32_t r_al;     // phase 2: rule index of the first staged rule word
+    uint32_t rstaged;  // phase 2: rule words staged in smem
+    uint32_t bases[kMaxSegPerStage];  // phase 1: segment base sources
+};
+static_assert(sizeof(StageHdr) <= kHdrBytes, "header fits");
+
+// Stage payload offsets (from the stage start)
+constexpr uint32_t kPayload = kHdrBytes;
+
+__device__ __forceinline__ uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// Stage descriptor (built on the host, build_tiles): 32 bytes.
+//   phase 1: {1 | last << 8, first segment, n segments, src0, P bytes, bases offset, 0, 0}
+//   phase 2: {2 | last << 8, first destination, n, r_al, rule bytes (0 = not staged), 0, 0, 0}
+struct StageDesc {
+    uint4 a, b;
+};
+
 template <int PM, bool WIDE>
-__global__ void __launch_bounds__(kTileThreads, 1) tiled_step_kernel(DevSys s, DevState st) {
-    extern __shared__ uint32_t acc[];  // [tile + 1]; slot `tile` absorbs nothing (dummy)
+__global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys s, DevState st) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* ring = smem;                                                     // kRingStages x kStageBytes
+    uint32_t* acc = reinterpret_cast<uint32_t*>(smem + kRingStages * kStageBytes);  // [tile + 1]
+    __shared__ __align__(8) uint64_t full_bar[kRingStages];
+    __shared__ __align__(8) uint64_t empty_bar[kRingStages];
+    __shared__ __align__(16) StageDesc desc_s[32];
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     const int halted = vc->halted;
@@ -727,7 +830,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tiled_step_kernel(DevSys s, D
     const StepCtx cx{k, slot, q, seed, Pcur, policy, record, sel, stats_on};
     const int T = s.tile;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int kWarps = kTileThreads / 32;
+    using Raw = typename RuleRaw<WIDE>::T;
 
     unsigned int stat[ST_COUNT];
 #pragma unroll
@@ -735,74 +838,186 @@ __global__ void __launch_bounds__(kTileThreads, 1) tiled_step_kernel(DevSys s, D
     bool t_fired = false, t_closed = false, t_neg = false;
     long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
 
-    for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
-        const long long d0 = tile * T;
-        const int nd = (int)min((long long)T, q - d0);
-        for (int i = threadIdx.x; i <= T; i += kTileThreads) acc[i] = 0;
-        __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kRingStages; ++b) {
+            mbar_init(&full_bar[b], 1);
+            mbar_init(&empty_bar[b], kWarpsC);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
 
-        // ---- phase 1: receive sums
-        const uint32_t g0 = __ldg(s.tseg + tile), g1 = __ldg(s.tseg + tile + 1);
-        for (uint32_t g = g0 + warp; g < g1; g += kWarps) {
-            const uint32_t base = __ldg(s.seg_base + g);
-            const uint4* wp = reinterpret_cast<const uint4*>(s.seg_words + (size_t)g * kSegEdges) + lane * 2;
-            const uint4 a = __ldg(wp), b = __ldg(wp + 1);
-            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            uint32_t v[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                v[e] = (w[e] != kDummyEdge) ? (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits)) : 0u;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                if (v[e]) atomicAdd(&acc[w[e] & ((1u << kDstBits) - 1u)], v[e]);
-                stat[ST_EDGES] += (w[e] != kDummyEdge) ? 1u : 0u;
+    if (warp == kWarpsC) {
+        // ================= producer warp: descriptors 32 at a time, lane 0 issues the TMA copies
+        uint32_t n_issued = 0;
+        const uint32_t rw_size = WIDE ? 16u : 8u;
+        for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
+            const long long d0 = tile * T;
+            const uint32_t s0 = __ldg(s.tstage + tile), s1 = __ldg(s.tstage + tile + 1);
+            for (uint32_t base = s0; base < s1; base += 32) {
+                // the warp loads 32 descriptors (coalesced) into shared memory;
+                // lane 0 alone walks them, so there is one warp sync per batch
+                const uint32_t cnt = min(32u, s1 - base);
+                if (lane < cnt) {
+                    desc_s[lane].a = __ldg(&s.stages[base + lane].a);
+                    desc_s[lane].b = __ldg(&s.stages[base + lane].b);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    for (uint32_t i = 0; i < cnt; ++i, ++n_issued) {
+                        const uint4 da = desc_s[i].a, db = desc_s[i].b;
+                        const uint32_t kind = da.x, first = da.y, n = da.z, f3 = da.w, f4 = db.x, f5 = db.y;
+                        const int b = n_issued % kRingStages;
+                        if (n_issued >= (uint32_t)kRingStages)
+                            mbar_wait(&empty_bar[b], ((n_issued / kRingStages) - 1) & 1u);
+                        fence_proxy_async_smem();
+                        uint8_t* buf = ring + b * kStageBytes;
+                        StageHdr* h = reinterpret_cast<StageHdr*>(buf);
+                        h->kind = kind & 0xff;
+                        h->last = kind >> 8;
+                        h->first = first;
+                        h->n = n;
+                        if ((kind & 0xff) == 1) {
+                            // f3 = src0, f4 = P bytes, f5 = bases offset
+                            const uint32_t wbytes = n * kSegEdges * 4u, bbytes = round16(n * 4u);
+                            h->src0 = f3;
+                            h->pstaged = f4 ? 1u : 0u;
+                            mbar_expect_tx(&full_bar[b], wbytes + f4 + bbytes);
+                            if (n) {
+                                bulk_g2s(h->bases, s.stage_bases + f5, bbytes, &full_bar[b]);
+                                bulk_g2s(buf + kPayload, s.seg_words + (size_t)first * kSegEdges, wbytes, &full_bar[b]);
+                            }
+                            if (f4) bulk_g2s(buf + kPayload + wbytes, Pprev + (f3 >> 5), f4, &full_bar[b]);
+                        } else {
+                            // f3 = r_al, f4 = staged rule bytes
+                            const long long j0 = d0 + first;
+                            const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u), b_roff = round16((n + 1u) * 4u);
+                            h->r_al = f3;
+                            h->rstaged = f4 ? 1u : 0u;
+                            mbar_expect_tx(&full_bar[b], b_cfg + b_ds + b_roff + f4);
+                            bulk_g2s(buf + kPayload, st.cfg + j0, b_cfg, &full_bar[b]);
+                            bulk_g2s(buf + kPayload + b_cfg, st.ds + j0, b_ds, &full_bar[b]);
+                            bulk_g2s(buf + kPayload + b_cfg + b_ds, s.roff + j0, b_roff, &full_bar[b]);
+                            if (f4)
+                                bulk_g2s(buf + kPayload + b_cfg + b_ds + b_roff,
+                                         reinterpret_cast<const uint8_t*>(s.rw) + (size_t)f3 * rw_size, f4, &full_bar[b]);
+                        }
+                    }
+                }
+                __syncwarp();
             }
         }
-        __syncthreads();
+    } else {
+        // ================= consumer warps
+        uint32_t cons = 0;
+        for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
+            const long long d0 = tile * T;
+            const int nd = (int)min((long long)T, q - d0);
+            for (int i = threadIdx.x; i <= T; i += kTileThreads) acc[i] = 0;
+            consumer_sync(kTileThreads);
 
-        // ---- phase 2: finish step k-1, select step k (light neurons)
-        const int nd32 = (nd + 31) & ~31;
-        for (int i = threadIdx.x; i < nd32; i += kTileThreads) {
-            const long long j = d0 + i;
-            const bool active = i < nd;
-            uint32_t r0 = 0, r1 = 0;
-            long long Cprev = 0;
-            int dsv = 0;
-            if (active) {
-                r0 = __ldg(s.roff + j);
-                r1 = __ldg(s.roff + j + 1);
-                Cprev = st.cfg[j];
-                dsv = st.ds[j];
-            }
-            const uint32_t nr = r1 - r0;
-            const bool heavy = active && nr > kLightRules;
-            int r = -1;
-            long long pval = 0;
-            if (active) {
-                const bool open_prev = ds_open(dsv);
-                const int D = ds_next(dsv);
-                const bool can_sel = sel && D == 0 && !heavy;
-                using Raw = typename RuleRaw<WIDE>::T;
-                Raw w0{}, w1{}, w2{}, w3{};
-                if (can_sel) {
-                    if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
-                    if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
-                    if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
-                    if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+            // ---- phase 1: receive sums
+            for (;;) {
+                const int b = cons % kRingStages;
+                const uint8_t* buf = ring + b * kStageBytes;
+                mbar_wait(&full_bar[b], (cons / kRingStages) & 1u);
+                ++cons;
+                const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+                const uint32_t n = h->n, last = h->last, src0 = h->src0;
+                const uint32_t* ps = reinterpret_cast<const uint32_t*>(buf + kPayload + n * kSegEdges * 4u);
+                for (uint32_t i = warp; i < n; i += kWarpsC) {
+                    // lane l takes edges l, l+32, ...: each instruction covers 32
+                    // consecutive (source-sorted) edges, so the P-bit loads hit
+                    // nearly consecutive words -- conflict-free shared loads
+                    const uint32_t base = h->bases[i];
+                    const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf + kPayload + i * kSegEdges * 4u) + lane;
+                    uint32_t w[8], v[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) w[e] = wp[e * 32];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const uint32_t src = base + (w[e] >> kDstBits);
+                        if (w[e] == kDummyEdge) {
+                            v[e] = 0u;
+                        } else if (PM == P_BIT) {
+                            const uint32_t rel = src - src0;
+                            v[e] = (ps[rel >> 5] >> (src & 31)) & 1u;
+                        } else {
+                            v[e] = (uint32_t)p_lookup<PM>(Pprev, src);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        if (v[e]) atomicAdd(&acc[w[e] & ((1u << kDstBits) - 1u)], v[e]);
+                        stat[ST_EDGES] += (w[e] != kDummyEdge) ? 1u : 0u;
+                    }
                 }
-                long long C = Cprev;
-                if (open_prev) {
-                    const uint32_t g = acc[i];
-                    C += (PM == P_BIT) ? (long long)g * s.p_common : (long long)g;
-                }
-                // heavy-rule neurons commit C_k / D_k here (no selection);
-                // phase 3 selects and overwrites
-                pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D,
-                                                                    can_sel, stat, t_fired, t_closed, t_neg, neg_idx,
-                                                                    neg_val, r);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[b]);
+                if (last) break;
             }
-            if (sel) {
-                if (PM == P_BIT) {
+            consumer_sync(kTileThreads);  // acc complete
+
+            // ---- phase 2: finish step k-1, select step k (one destination per thread)
+            for (;;) {
+                const int b = cons % kRingStages;
+                const uint8_t* buf = ring + b * kStageBytes;
+                mbar_wait(&full_bar[b], (cons / kRingStages) & 1u);
+                ++cons;
+                const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+                const uint32_t n = h->n, last = h->last, first = h->first, r_al = h->r_al;
+                const bool rstaged = h->rstaged != 0;
+                const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u), b_roff = round16((n + 1u) * 4u);
+                const long long* cfg_s = reinterpret_cast<const long long*>(buf + kPayload);
+                const int* ds_s = reinterpret_cast<const int*>(buf + kPayload + b_cfg);
+                const uint32_t* roff_s = reinterpret_cast<const uint32_t*>(buf + kPayload + b_cfg + b_ds);
+                const Raw* rules_s = reinterpret_cast<const Raw*>(buf + kPayload + b_cfg + b_ds + b_roff);
+                const int li = threadIdx.x;
+                const int i = (int)first + li;
+                const long long j = d0 + i;
+                const bool active = li < (int)n;
+                uint32_t r0 = 0, r1 = 0;
+                long long Cprev = 0;
+                int dsv = 0;
+                if (active) {
+                    r0 = roff_s[li];
+                    r1 = roff_s[li + 1];
+                    Cprev = cfg_s[li];
+                    dsv = ds_s[li];
+                }
+                const uint32_t nr = r1 - r0;
+                const bool heavy = active && nr > kLightRules;
+                int r = -1;
+                long long pval = 0;
+                if (active) {
+                    const bool open_prev = ds_open(dsv);
+                    const int D = ds_next(dsv);
+                    const bool can_sel = sel && D == 0 && !heavy;
+                    Raw w0{}, w1{}, w2{}, w3{};
+                    if (can_sel) {
+                        if (rstaged) {
+                            const Raw* rp = rules_s + (r0 - r_al);
+                            if (nr > 0) w0 = rp[0];
+                            if (nr > 1) w1 = rp[1];
+                            if (nr > 2) w2 = rp[2];
+                            if (nr > 3) w3 = rp[3];
+                        } else {
+                            if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                            if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                            if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                            if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                        }
+                    }
+                    long long C = Cprev;
+                    if (open_prev) {
+                        const uint32_t gsum = acc[i];
+                        C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
+                    }
+                    pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3,
+                                                                        C, D, can_sel, stat, t_fired, t_closed, t_neg,
+                                                                        neg_idx, neg_val, r);
+                }
+                if (sel && PM == P_BIT) {
                     const unsigned int bits = __ballot_sync(0xffffffffu, pval > 0);
                     const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
                     const unsigned int act = __ballot_sync(0xffffffffu, active);
@@ -816,80 +1031,84 @@ __global__ void __launch_bounds__(kTileThreads, 1) tiled_step_kernel(DevSys s, D
                         }
                     }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[b]);
+                if (last) break;
             }
-        }
+            consumer_sync(kTileThreads);  // phase-2 commits visible; acc free after phase 3
 
-        // ---- phase 3: heavy-rule neurons of this tile, one warp each
-        const uint32_t h0 = __ldg(s.theavy + tile), h1 = __ldg(s.theavy + tile + 1);
-        if (sel && h1 > h0) {
-            __syncthreads();  // phase-2 commits of C_k / D_k are visible CTA-wide
-            for (uint32_t h = h0 + warp; h < h1; h += kWarps) {
-                const long long j = s.heavy[h];
-                const int D = st.ds[j];  // phase 2 stored D_k (>= 0, not fired)
-                if (D != 0) continue;
-                const long long C = st.cfg[j];
-                const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
-                int r = -1;
-                if (policy == 0) {
-                    for (uint32_t base = r0; base < r1 && r < 0; base += 32) {
-                        const uint32_t t = base + lane;
-                        const unsigned int b =
-                            __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
-                        if (b) r = (int)(base + __ffs(b) - 1);
-                    }
-                    if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
-                } else {
-                    uint32_t total = 0;
-                    for (uint32_t base = r0; base < r1; base += 32) {
-                        const uint32_t t = base + lane;
-                        total += __popc(__ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C)));
-                    }
-                    if (lane == 0) stat[ST_SCANNED] += r1 - r0;
-                    if (total) {
-                        uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
-                        for (uint32_t base = r0; base < r1; base += 32) {
-                            const uint32_t t = base + lane;
-                            const unsigned int b =
+            // ---- phase 3: heavy-rule neurons of this tile, one warp each
+            const uint32_t h0 = __ldg(s.theavy + tile), h1 = __ldg(s.theavy + tile + 1);
+            if (sel && h1 > h0) {
+                for (uint32_t hh = h0 + warp; hh < h1; hh += kWarpsC) {
+                    const long long j = s.heavy[hh];
+                    const int D = st.ds[j];  // phase 2 stored D_k (>= 0, not fired)
+                    if (D != 0) continue;
+                    const long long C = st.cfg[j];
+                    const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
+                    int r = -1;
+                    if (policy == 0) {
+                        for (uint32_t rb = r0; rb < r1 && r < 0; rb += 32) {
+                            const uint32_t t = rb + lane;
+                            const unsigned int bb =
                                 __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
-                            const uint32_t c = __popc(b);
-                            if (want < c) {
-                                r = (int)(base + nth_set_bit(b, want));
-                                break;
+                            if (bb) r = (int)(rb + __ffs(bb) - 1);
+                        }
+                        if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
+                    } else {
+                        uint32_t total = 0;
+                        for (uint32_t rb = r0; rb < r1; rb += 32) {
+                            const uint32_t t = rb + lane;
+                            total += __popc(
+                                __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C)));
+                        }
+                        if (lane == 0) stat[ST_SCANNED] += r1 - r0;
+                        if (total) {
+                            uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
+                            for (uint32_t rb = r0; rb < r1; rb += 32) {
+                                const uint32_t t = rb + lane;
+                                const unsigned int bb =
+                                    __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
+                                const uint32_t c = __popc(bb);
+                                if (want < c) {
+                                    r = (int)(rb + nth_set_bit(bb, want));
+                                    break;
+                                }
+                                want -= c;
                             }
-                            want -= c;
+                        }
+                    }
+                    if (lane == 0) {
+                        stat[ST_OPEN] += 1;
+                        if (r >= 0) {
+                            const uint4 wr = load_rule<WIDE>(s.rw, r);
+                            st.cfg[j] = C - (long long)wr.y;
+                            st.ds[j] = -((int)wr.w + 1);
+                            t_fired = true;
+                            stat[ST_FIRED] += 1;
+                            if (wr.z > 0) {
+                                stat[ST_SENDING] += 1;
+                                if (stats_on) {
+                                    const uint32_t od = __ldg(s.outdeg + j);
+                                    stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
+                                }
+                            }
+                            if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
+                            if (PM == P_BIT) {
+                                if (wr.z > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
+                            } else if (PM == P_U8) {
+                                reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)wr.z;
+                            } else if (PM == P_U16) {
+                                reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)wr.z;
+                            } else {
+                                Pcur[j] = wr.z;
+                            }
                         }
                     }
                 }
-                if (lane == 0) {
-                    stat[ST_OPEN] += 1;
-                    if (r >= 0) {
-                        const uint4 wr = load_rule<WIDE>(s.rw, r);
-                        st.cfg[j] = C - (long long)wr.y;
-                        st.ds[j] = -((int)wr.w + 1);
-                        t_fired = true;
-                        stat[ST_FIRED] += 1;
-                        if (wr.z > 0) {
-                            stat[ST_SENDING] += 1;
-                            if (stats_on) {
-                                const uint32_t od = __ldg(s.outdeg + j);
-                                stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
-                            }
-                        }
-                        if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
-                        if (PM == P_BIT) {
-                            if (wr.z > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
-                        } else if (PM == P_U8) {
-                            reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)wr.z;
-                        } else if (PM == P_U16) {
-                            reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)wr.z;
-                        } else {
-                            Pcur[j] = wr.z;
-                        }
-                    }
-                }
+                consumer_sync(kTileThreads);
             }
         }
-        __syncthreads();  // acc is reused by the next tile
     }
 
     if (stats_on) flush_stats(ctl, stat);

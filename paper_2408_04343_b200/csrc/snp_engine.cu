@@ -150,7 +150,8 @@ int grid_for(long long n, int block = 256) {
 // CSR out-adjacency is source-major, so a stable bucket pass keeps that
 // order), are packed into 256-edge segments whose sources span < 2^17.
 int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff,
-                const std::vector<uint32_t>& sdst, std::vector<uint32_t>& heavy) {
+                const std::vector<uint32_t>& sdst, const std::vector<uint32_t>& roff_h,
+                std::vector<uint32_t>& heavy) {
     const long long q = e->q;
     DevSys& s = e->sys;
     int n_sm = 148;
@@ -159,10 +160,17 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     heavy.clear();
     for (long long i = 0; i < q; ++i)
         if (d->offsets[i + 1] - d->offsets[i] > (long long)kLightRules) heavy.push_back((uint32_t)i);
+    // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
     long long T = ceil_div(std::max<long long>(q, 1), 4ll * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
     if (const char* env = getenv("SNPB200_TILE")) T = atoll(env);
-    T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
+    // shared memory: the TMA ring plus one 32-bit counter per destination
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
+    const long long t_smem = ((long long)smem_optin - (long long)kRingStages * kStageBytes - 1024) / 4 - 1;
+    T = std::min<long long>(std::min<long long>(kMaxTile, t_smem), std::max<long long>(32, (T + 31) / 32 * 32));
+    T = T / 32 * 32;
+    if (T < 32) return fail(SNP_ERR_CAPACITY, "not enough shared memory for the tiled kernel");
     const long long n_tiles = std::max<long long>(1, ceil_div(q, T));
     s.tile = (int)T;
     s.n_tiles = n_tiles;
@@ -182,7 +190,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
             bslot[pos] = (uint16_t)(dst % T);
         }
     // segments
-    std::vector<uint32_t> tseg(n_tiles + 1, 0), base;
+    std::vector<uint32_t> tseg(n_tiles + 1, 0), base, last;
     std::vector<uint32_t> words;
     words.reserve((size_t)(S + S / 8 + 256));
     for (long long t = 0; t < n_tiles; ++t) {
@@ -197,11 +205,68 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
                 ++e2;
                 ++n;
             }
+            last.push_back(bsrc[e2 - 1]);
             for (; n < kSegEdges; ++n) words.push_back(kDummyEdge);
         }
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
     }
+    // TMA stage descriptors (see tiled_step_kernel): phase-1 stages take as
+    // many consecutive segments as fit with the P window they reference,
+    // phase-2 stages kSub destinations with (when they fit) their rule words
+    std::vector<StageDesc> desc;
+    std::vector<uint32_t> tstage(n_tiles + 1, 0), sbases;
+    const uint32_t rw_size = e->wide_rules ? 16u : 8u;
+    auto r16 = [](unsigned long long x) { return (uint32_t)((x + 15) & ~15ull); };
+    for (long long t = 0; t < n_tiles; ++t) {
+        uint32_t g = tseg[t];
+        const uint32_t g1 = tseg[t + 1];
+        do {
+            uint32_t n = 0, src0 = 0, pbytes = 0;
+            if (g < g1) {
+                src0 = base[g] & ~127u;
+                while (g + n < g1 && n < kMaxSegPerStage) {
+                    const uint32_t pb = e->p_mode == P_BIT ? r16((last[g + n] + 1u - src0 + 7u) / 8u) : 0u;
+                    if (kPayload + (n + 1) * kSegEdges * 4u + pb > kStageBytes) break;
+                    pbytes = pb;
+                    ++n;
+                }
+            }
+            const uint32_t boff = (uint32_t)sbases.size();
+            for (uint32_t i = 0; i < n; ++i) sbases.push_back(base[g + i]);
+            while (sbases.size() % 4) sbases.push_back(0);
+            StageDesc sd;
+            sd.a = make_uint4(1u | ((g + n >= g1) ? 256u : 0u), g, n, src0);
+            sd.b = make_uint4(pbytes, boff, 0, 0);
+            desc.push_back(sd);
+            g += n;
+        } while (g < g1);
+        const long long d0 = t * T;
+        const long long nd = std::min<long long>(T, q - d0);
+        for (long long dd = 0; dd < nd; dd += kSub) {
+            const uint32_t n = (uint32_t)std::min<long long>(kSub, nd - dd);
+            const uint32_t rf = roff_h[d0 + dd], rl = roff_h[d0 + dd + n];
+            const uint32_t r_al = e->wide_rules ? rf : (rf & ~1u);
+            const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + r16((n + 1) * 4ull);
+            uint32_t rb = r16((unsigned long long)(rl - r_al) * rw_size);
+            if (fixed + rb > kStageBytes) rb = 0;
+            StageDesc sd;
+            sd.a = make_uint4(2u | ((dd + kSub >= nd) ? 256u : 0u), (uint32_t)dd, n, r_al);
+            sd.b = make_uint4(rb, 0, 0, 0);
+            desc.push_back(sd);
+        }
+        tstage[t + 1] = (uint32_t)desc.size();
+    }
+    StageDesc* d_desc;
+    uint32_t *d_tstage, *d_sbases;
+    TRY(upload(e, &d_desc, desc));
+    TRY(upload(e, &d_tstage, tstage));
+    sbases.resize(sbases.size() + 4, 0);
+    TRY(upload(e, &d_sbases, sbases));
+    s.stages = d_desc;
+    s.tstage = d_tstage;
+    s.stage_bases = d_sbases;
+
     // heavy-rule neurons per tile (heavy is ascending)
     std::vector<uint32_t> theavy(n_tiles + 1, 0);
     for (uint32_t hn : heavy) theavy[hn / T + 1]++;
@@ -239,7 +304,8 @@ int build(snp_engine* e, const snp_system_desc* d) {
 
     // --- rule vector + offsets (matrices.py:48-73, 115-140)
     if (q > 0 && d->offsets[0] != 0) return fail(SNP_ERR_BAD_ARG, "offsets[0] must be 0");
-    std::vector<uint32_t> roff(q + 1, 0), owner(m);
+    // +8 tail: the TMA stages of the tiled kernel copy whole 16-byte units
+    std::vector<uint32_t> roff(q + 1 + 8, 0), owner(m);
     for (long long i = 0; i < q; ++i) {
         const long long a = d->offsets[i], b = d->offsets[i + 1];
         if (b < a || b > m) return fail(SNP_ERR_BAD_ARG, "offsets not non-decreasing within [0, m]");
@@ -385,14 +451,14 @@ int build(snp_engine* e, const snp_system_desc* d) {
     s.outdeg = d_outdeg;
     e->wide_rules = !compact;
     if (compact) {
-        std::vector<uint2> rw(m);
+        std::vector<uint2> rw(m + 2);  // +2: 16-byte bulk-copy tails
         for (long long r = 0; r < m; ++r)
             rw[r] = make_uint2(rthr[r], (uint32_t)rrec[r].x | ((uint32_t)rrec[r].y << 16) | ((uint32_t)rrec[r].z << 24));
         uint2* d_rw;
         TRY(upload(e, &d_rw, rw));
         s.rw = d_rw;
     } else {
-        std::vector<uint4> rw(m);
+        std::vector<uint4> rw(m + 1);
         for (long long r = 0; r < m; ++r)
             rw[r] = make_uint4(rthr[r], (uint32_t)rrec[r].x, (uint32_t)rrec[r].y, (uint32_t)rrec[r].z);
         uint4* d_rw;
@@ -450,7 +516,7 @@ int build(snp_engine* e, const snp_system_desc* d) {
         const bool many_in = e->kind == RECV_PULL && !e->tiled && ((indeg[i] + 3u) & ~3u) > kLightIn;
         if (many_rules || many_in) heavy.push_back((uint32_t)i);
     }
-    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, heavy));
+    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, roff, heavy));
     uint32_t* d_heavy;
     TRY(upload(e, &d_heavy, heavy));
     s.heavy = d_heavy;
@@ -509,13 +575,13 @@ int build(snp_engine* e, const snp_system_desc* d) {
     }
 
     // --- run state
-    TRY(e->alloc(&st.cfg, q));
-    TRY(e->alloc(&st.ds, q));
+    TRY(e->alloc(&st.cfg, q + 8));  // +8: 16-byte bulk-copy tails
+    TRY(e->alloc(&st.ds, q + 8));
     TRY(e->alloc(&st.chosen, q));
     if (e->kind == RECV_PULL) {
         long long words;
         switch (e->p_mode) {
-            case P_BIT: words = ceil_div(q + 1, 32) + 1; break;
+            case P_BIT: words = ceil_div(q + 1, 32) + 8; break;  // +8: bulk-copy tails
             case P_U8: words = ceil_div(q + 1, 4) + 1; break;
             case P_U16: words = ceil_div(q + 1, 2) + 1; break;
             default: words = q + 2; break;
@@ -560,10 +626,10 @@ int build(snp_engine* e, const snp_system_desc* d) {
     int per_sm = 0, n_sm = 0;
     CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, e->device));
     if (e->tiled) {
-        e->step_block = kTileThreads;
-        e->step_smem = (size_t)(s.tile + 1) * sizeof(uint32_t);
+        e->step_block = kTileThreads + 32;  // consumer warps + one TMA producer warp
+        e->step_smem = (size_t)kRingStages * kStageBytes + (size_t)(s.tile + 1) * sizeof(uint32_t);
         CU(cudaFuncSetAttribute(e->step_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, kTileThreads, e->step_smem));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, e->step_block, e->step_smem));
         const long long resident = (long long)std::max(1, per_sm) * std::max(1, n_sm);
         e->step_grid = (int)std::min<long long>(s.n_tiles, resident);
         e->resident_ctas = resident;
@@ -620,7 +686,7 @@ int reset_state(snp_engine* e) {
         for (int i = 0; i < 3; ++i) {
             size_t bytes;
             switch (e->p_mode) {
-                case P_BIT: bytes = (ceil_div(q + 1, 32) + 1) * 4; break;
+                case P_BIT: bytes = (ceil_div(q + 1, 32) + 8) * 4; break;
                 case P_U8: bytes = (ceil_div(q + 1, 4) + 1) * 4; break;
                 case P_U16: bytes = (ceil_div(q + 1, 2) + 1) * 4; break;
                 default: bytes = (q + 2) * 4; break;
@@ -815,8 +881,10 @@ int snp_advance(snp_engine* e, const snp_run_opts* o, int64_t n_steps, snp_trace
             for (long long i = 0; i < seg; ++i) launches += launch_step(e);
             CU(cudaGetLastError());
         }
+        CU(cudaGetLastError());
         TRY(pull_ctrl(e));
-        const long long k1 = c.halted ? c.step : c.step;  // halt step or next step
+        const long long k1 = c.step;  // halt step or next step
+        if (k1 == k0 && !c.halted) return fail(SNP_ERR_CUDA, "device loop made no progress at step %lld", k0);
         long long cfg_rows = c.halted ? (k1 - k0 + 1) : (k1 - k0);
         long long sp_rows = k1 - k0;
         if (c.halted && c.reason == HALT_NEGATIVE) break;
@@ -921,6 +989,7 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
                 }
             }
         }
+        CU(cudaGetLastError());
         CU(cudaEventRecord(e->ev1, e->stream));
         CU(cudaEventSynchronize(e->ev1));
         double sum = 0;
