@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--workload", choices=["k3", "k4", "k2"], default="k3")
     p.add_argument("--q", type=int, default=Q_K3)
     p.add_argument("--format", choices=["compressed", "ell", "sparse"], default="compressed")
-    p.add_argument("--variant", choices=["pull", "push"], default="pull")
+    p.add_argument("--variant", choices=["tiled", "pull", "push"], default="tiled")
     p.add_argument("--policy", choices=["first", "seeded"], default="first")
     p.add_argument("--extra", action="store_true", help="also measure the other formats/policies")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -193,11 +193,15 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
     launches = int(res.kernel_launches)
 
-    # per-kernel durations + exact traffic counters (separate, untimed pass)
+    # per-launch durations of the step kernel (CUDA events around each launch)
     eng.begin()
     eng.time_steps(args.warmup, sel)
     nk = min(args.steps, 50)
-    _, kernel_ms, res_k = eng.time_steps(nk, sel, per_kernel=True, collect_stats=True)
+    _, kernel_ms, _ = eng.time_steps(nk, sel, per_kernel=True)
+    # exact traffic counters of the same steps (separate pass: counting costs atomics)
+    eng.begin()
+    eng.time_steps(args.warmup, sel)
+    _, _, res_k = eng.time_steps(nk, sel, collect_stats=True)
     stats = res_k.stats_dict()
     alg = algorithmic_bytes(args.format, q, m, stats, nk)
 
@@ -340,9 +344,10 @@ def extra_measurements(args) -> dict:
     """Other formats / policies / K4 on the same box (not the headline)."""
     import paper_2408_04343_b200 as snp
     out = {}
-    cases = [("k3", "compressed", "push", "first"), ("k3", "ell", "pull", "first"),
-             ("k3", "compressed", "pull", "seeded"), ("k4", "compressed", "pull", "first"),
-             ("k4", "compressed", "pull", "seeded")]
+    cases = [("k3", "compressed", "pull", "first"), ("k3", "compressed", "push", "first"),
+             ("k3", "ell", "push", "first"), ("k3", "compressed", "tiled", "seeded"),
+             ("k4", "compressed", "tiled", "first"), ("k4", "compressed", "tiled", "seeded"),
+             ("k2", "compressed", "tiled", "first"), ("k2", "compressed", "pull", "first")]
     for wl, fmt, var, pol in cases:
         a2 = argparse.Namespace(**vars(args))
         a2.workload, a2.format, a2.variant, a2.policy = wl, fmt, var, pol
@@ -355,10 +360,14 @@ def extra_measurements(args) -> dict:
         tot, _, _ = eng.time_steps(args.steps, sel)
         eng.begin()
         eng.time_steps(args.warmup, sel)
-        _, kms, res = eng.time_steps(30, sel, per_kernel=True, collect_stats=True)
+        _, kms, _ = eng.time_steps(30, sel, per_kernel=True)
+        eng.begin()
+        eng.time_steps(args.warmup, sel)
+        _, _, res = eng.time_steps(30, sel, collect_stats=True)
         alg = algorithmic_bytes(fmt, arrays.neuron_count, arrays.rule_count, res.stats_dict(), 30)
-        out[f"{wl}/{fmt}/{var}/{pol}"] = {"steps_per_s": args.steps / (tot / 1000), "ms_per_step": tot / args.steps,
-                                          "step_kernel_ms": kms, "alg_GBps_step_kernel": alg / (kms / 1000) / 1e9}
+        ms = tot / args.steps
+        out[f"{wl}/{fmt}/{var}/{pol}"] = {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "step_kernel_ms": kms,
+                                          "alg_bytes_per_step": alg, "alg_GBps_per_step": alg / (ms / 1000) / 1e9}
         del prep, eng
     return out
 

@@ -1001,15 +1001,19 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
         for (auto& x : ev) cudaEventDestroy(x);
         *kernel_ms = steps > 0 ? sum / steps : 0.0;
     } else {
+        // whole graph replays of `chunk` steps, the remainder launched directly:
+        // exactly `steps` step iterations are enqueued
         const long long chunk = std::min<long long>((long long)steps, 64ll);
-        TRY(ensure_graph(e, chunk));
+        if (chunk > 0) TRY(ensure_graph(e, chunk));
         CU(cudaEventRecord(e->ev0, e->stream));
         long long done = 0;
-        while (done < steps) {
+        while (chunk > 0 && done + chunk <= steps) {
             CU(cudaGraphLaunch(e->graph, e->stream));
             launches += chunk * kernels_per_step(e);
             done += chunk;
         }
+        for (; done < steps; ++done) launches += launch_step(e);
+        CU(cudaGetLastError());
         CU(cudaEventRecord(e->ev1, e->stream));
         CU(cudaEventSynchronize(e->ev1));
     }
