@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SNPB200_ABI_VERSION 1
+#define SNPB200_ABI_VERSION 2
 
 enum {
     SNP_OK = 0,
@@ -85,6 +85,8 @@ typedef struct snp_system_desc {
     int64_t ell_rows;
     const int64_t *sparse_data;  /* SparseMatrix.data [m][q] (matrices.py:76-80) */
     int32_t device;              /* CUDA ordinal */
+    int32_t world;               /* row partition: ranks (0 or 1 = whole system) */
+    int32_t rank;                /* row partition: this engine's rank */
     int32_t reserved;
 } snp_system_desc;
 
@@ -176,6 +178,38 @@ int snp_step(snp_engine *eng, const int64_t *config, const int64_t *delays,
              const int64_t *chosen, int64_t *next_config, int64_t *row_visits);
 int snp_update_delays(snp_engine *eng, const int64_t *delays, const int64_t *chosen,
                       int64_t *next_delays);
+
+/* Row partition (multi-GPU).  An engine created with
+ * world > 1 owns neurons [lo, hi) of the q-neuron system, COMPRESSED only,
+ * with nl = round_up(ceil(q / world), 128), lo = rank * nl, hi = min(q, lo + nl).
+ * In the descriptor, `q` is the whole system, the node arrays (initial,
+ * offsets, rule vector, `m`) describe neurons [lo, hi) only, and
+ * adj_offsets/adj_targets is a CSR over all q sources that must contain every
+ * edge entering [lo, hi) (other edges are ignored).  Each step kernel
+ * publishes the rank's production bits and step flags into its chunk of the
+ * current exchange slot; the caller must all-gather that slot across ranks
+ * (in place: chunk at chunk_offset_bytes of a slot_bytes buffer) before the
+ * next snp_launch_step.  Step k writes slot k % 3. */
+typedef struct snp_exchange {
+    void *slot[3];               /* device pointers of the three exchange slots */
+    int64_t slot_bytes;          /* bytes all-gathered per slot */
+    int64_t chunk_offset_bytes;  /* this rank's chunk within a slot */
+    int64_t chunk_bytes;
+    int64_t lo, hi;              /* owned global neurons */
+    int64_t neurons_per_rank;
+    int32_t world, rank;
+} snp_exchange;
+
+int snp_exchange_info(const snp_engine *eng, snp_exchange *x);
+/* Launch on the caller's CUDA stream (cudaStream_t passed as void*; NULL =
+ * the engine's own stream), e.g. the stream NCCL runs on. */
+int snp_set_stream(snp_engine *eng, void *stream);
+/* After snp_begin: run parameters for snp_launch_step. */
+int snp_configure(snp_engine *eng, const snp_run_opts *opts);
+/* Enqueue one step (no host synchronisation). */
+int snp_launch_step(snp_engine *eng);
+/* Synchronise the engine stream and read the run state. */
+int snp_poll(snp_engine *eng, snp_result *res);
 
 /* Timing helper for benchmarks: run `steps` steps (no recording) from the
  * current state with the device loop only and return the per-kernel mean

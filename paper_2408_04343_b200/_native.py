@@ -38,7 +38,8 @@ class SystemDesc(ctypes.Structure):
         ("syn_target", _i64p), ("syn_rows", ctypes.c_int64),
         ("ell_target", _i64p), ("ell_amount", _i64p), ("ell_rows", ctypes.c_int64),
         ("sparse_data", _i64p),
-        ("device", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("device", ctypes.c_int32), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -79,6 +80,14 @@ class EngineInfo(ctypes.Structure):
     ]
 
 
+class Exchange(ctypes.Structure):
+    _fields_ = [
+        ("slot", ctypes.c_void_p * 3), ("slot_bytes", ctypes.c_int64), ("chunk_offset_bytes", ctypes.c_int64),
+        ("chunk_bytes", ctypes.c_int64), ("lo", ctypes.c_int64), ("hi", ctypes.c_int64),
+        ("neurons_per_rank", ctypes.c_int64), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+    ]
+
+
 # (name, restype, argtypes) -- every symbol include/snpb200.h declares
 _EngineP = ctypes.c_void_p
 SIGNATURES = [
@@ -100,6 +109,11 @@ SIGNATURES = [
     ("snp_step", ctypes.c_int, [_EngineP, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_void_p]),
     ("snp_update_delays", ctypes.c_int, [_EngineP, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("snp_exchange_info", ctypes.c_int, [_EngineP, ctypes.POINTER(Exchange)]),
+    ("snp_set_stream", ctypes.c_int, [_EngineP, ctypes.c_void_p]),
+    ("snp_configure", ctypes.c_int, [_EngineP, ctypes.POINTER(RunOpts)]),
+    ("snp_launch_step", ctypes.c_int, [_EngineP]),
+    ("snp_poll", ctypes.c_int, [_EngineP, ctypes.POINTER(Result)]),
     ("snp_time_steps", ctypes.c_int, [_EngineP, ctypes.POINTER(RunOpts), ctypes.c_int64,
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(Result)]),

@@ -124,6 +124,14 @@ struct DevSys {
     const uint32_t* theavy;     // [n_tiles + 1] range of s.heavy inside each tile
     int tile;                   // destinations per tile (multiple of 32)
     long long n_tiles;
+    // row partition (sharded.py): local neuron j is global neuron gbase + j and
+    // publishes its P bit at exchange-space position xbase + j; rank r's chunk
+    // is x_stride words, the last 4 of which carry its step flags
+    long long gbase;
+    long long xbase;
+    long long x_stride;         // words per rank chunk (0 = not sharded)
+    int world;
+    int rank;
 };
 
 struct DevState {
@@ -246,7 +254,8 @@ __device__ __forceinline__ void flush_stats(Ctrl* ctl, unsigned int (&loc)[ST_CO
 // Last-CTA-done: halting decision for step k (engine.py:443-450) and reset
 // of the per-step flags.  Called by thread 0 of every CTA.
 __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bool bf, bool bc,
-                                            bool bn, long long neg_idx, long long neg_val) {
+                                            bool bn, long long neg_idx, long long neg_val,
+                                            uint32_t* xhdr = nullptr) {
     if (bf) atomicOr(&ctl->fired_any, 1);
     if (bc) atomicOr(&ctl->closed_any, 1);
     if (bn) {
@@ -267,6 +276,25 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
     v->list_count[(k + 1) & 1] = 0;
     v->heavy_count[(k + 1) & 1] = 0;
     int armed = 0;
+    if (xhdr) {
+        // row partition: publish this rank's flags with its P chunk; every
+        // rank takes the same decision at the start of the next step kernel
+        volatile uint32_t* h = xhdr;
+        h[0] = (uint32_t)fired;
+        h[1] = (uint32_t)closed;
+        h[2] = (uint32_t)neg;
+        h[3] = 0u;
+        if (!sel) {
+            v->halted = 1;
+            v->reason = HALT_STEP_LIMIT;
+        } else {
+            v->step = k + 1;
+            if (v->stats_on) v->stats[ST_STEPS] += 1;
+        }
+        v->push_armed = 0;
+        __threadfence();
+        return;
+    }
     if (neg) {
         v->halted = 1;
         v->reason = HALT_NEGATIVE;
@@ -374,7 +402,7 @@ __device__ __forceinline__ long long light_commit(const DevSys& s, const DevStat
     long long pval = 0;
     if (C < 0) {
         t_neg = true;
-        neg_idx = j;
+        neg_idx = j + s.gbase;
         neg_val = C;
     }
     if (cx.record & REC_CONFIGS) st.tr_cfg[cx.slot * cx.q + j] = C;
@@ -395,7 +423,7 @@ __device__ __forceinline__ long long light_commit(const DevSys& s, const DevStat
                 idx = __ffs(mask) - 1;
                 stat[ST_SCANNED] += idx + 1;
             } else {
-                idx = nth_set_bit(mask, (uint32_t)(mix64(cx.seed, cx.k, j) % (uint32_t)__popc(mask)));
+                idx = nth_set_bit(mask, (uint32_t)(mix64(cx.seed, cx.k, j + s.gbase) % (uint32_t)__popc(mask)));
                 stat[ST_SCANNED] += nr;
             }
             r = (int)(r0 + idx);
@@ -431,9 +459,9 @@ __device__ __forceinline__ long long light_commit(const DevSys& s, const DevStat
         if (KIND == RECV_ARRAY) st.chosen[j] = r;
         if (cx.record & REC_SPIKING) st.tr_chosen[cx.slot * cx.q + j] = r;
         if (KIND == RECV_PULL && PM != P_BIT) {
-            if (PM == P_U8) reinterpret_cast<uint8_t*>(cx.Pcur)[j] = (uint8_t)pval;
-            else if (PM == P_U16) reinterpret_cast<uint16_t*>(cx.Pcur)[j] = (uint16_t)pval;
-            else cx.Pcur[j] = (uint32_t)pval;
+            if (PM == P_U8) reinterpret_cast<uint8_t*>(cx.Pcur)[j + s.xbase] = (uint8_t)pval;
+            else if (PM == P_U16) reinterpret_cast<uint16_t*>(cx.Pcur)[j + s.xbase] = (uint16_t)pval;
+            else cx.Pcur[j + s.xbase] = (uint32_t)pval;
         }
     }
     return pval;
@@ -817,6 +845,28 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->push_armed = 0;
         return;
     }
+    if (s.x_stride && k > 0) {
+        // row partition: halting decision for step k-1 from every rank's flags
+        // (all-gathered with P_{k-1}); identical on every rank
+        const volatile uint32_t* Pg = pick3(st.P, (k + 2) % 3);
+        uint32_t f = 0, c = 0, n = 0;
+        for (int r = 0; r < s.world; ++r) {
+            const volatile uint32_t* h = Pg + (long long)r * s.x_stride + s.x_stride - 4;
+            f |= h[0];
+            c |= h[1];
+            n |= h[2];
+        }
+        if (n || (!f && !c)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                ctl->halted = 1;
+                ctl->reason = n ? HALT_NEGATIVE : HALT_NO_APPLICABLE;
+                if (!n) ctl->step = k - 1;
+                ctl->neg_any = n ? 1 : 0;
+                ctl->push_armed = 0;
+            }
+            return;
+        }
+    }
     const bool sel = k < vc->max_steps;
     const int policy = vc->policy;
     const unsigned long long seed = vc->seed;
@@ -1022,7 +1072,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
                     const unsigned int act = __ballot_sync(0xffffffffu, active);
                     if (lane == 0 && act) {
-                        const long long wd = j >> 5;
+                        const long long wd = (j + s.xbase) >> 5;
                         Pzero[wd] = 0u;
                         if (hv) {
                             if (bits) atomicOr(Pcur + wd, bits);
@@ -1064,7 +1114,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                         }
                         if (lane == 0) stat[ST_SCANNED] += r1 - r0;
                         if (total) {
-                            uint32_t want = (uint32_t)(mix64(seed, k, j) % total);
+                            uint32_t want = (uint32_t)(mix64(seed, k, j + s.gbase) % total);
                             for (uint32_t rb = r0; rb < r1; rb += 32) {
                                 const uint32_t t = rb + lane;
                                 const unsigned int bb =
@@ -1094,14 +1144,15 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                                 }
                             }
                             if (record & REC_SPIKING) st.tr_chosen[slot * q + j] = r;
+                            const long long jx = j + s.xbase;
                             if (PM == P_BIT) {
-                                if (wr.z > 0) atomicOr(Pcur + (j >> 5), 1u << (j & 31));
+                                if (wr.z > 0) atomicOr(Pcur + (jx >> 5), 1u << (jx & 31));
                             } else if (PM == P_U8) {
-                                reinterpret_cast<uint8_t*>(Pcur)[j] = (uint8_t)wr.z;
+                                reinterpret_cast<uint8_t*>(Pcur)[jx] = (uint8_t)wr.z;
                             } else if (PM == P_U16) {
-                                reinterpret_cast<uint16_t*>(Pcur)[j] = (uint16_t)wr.z;
+                                reinterpret_cast<uint16_t*>(Pcur)[jx] = (uint16_t)wr.z;
                             } else {
-                                Pcur[j] = wr.z;
+                                Pcur[jx] = wr.z;
                             }
                         }
                     }
@@ -1121,7 +1172,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     __syncthreads();
     if (t_neg && sh_neg_idx == neg_idx) sh_neg_val = neg_val;
     const bool bn = __syncthreads_or(t_neg);
-    if (threadIdx.x == 0) finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0);
+    if (threadIdx.x == 0)
+        finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0,
+                    s.x_stride ? Pcur + (long long)s.rank * s.x_stride + s.x_stride - 4 : nullptr);
 }
 
 // ---------------------------------------------------------------------------

@@ -73,6 +73,9 @@ struct snp_engine {
     long long in_edges = 0;
     int kind = RECV_PULL;
     bool tiled = false;
+    long long p_words = 0;  // sharded: exchange words per P buffer
+    long long shard_lo = 0, shard_hi = 0, shard_nl = 0;
+    cudaStream_t own_stream = nullptr;
     int step_block = kBlock;
     size_t step_smem = 0;
     bool wide_rules = false;
@@ -122,7 +125,7 @@ struct snp_engine {
         for (void* p : allocs) cudaFree(p);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
-        if (stream) cudaStreamDestroy(stream);
+        if (own_stream) cudaStreamDestroy(own_stream);
     }
 };
 
@@ -145,13 +148,29 @@ int grid_for(long long n, int block = 256) {
     return (int)std::max<long long>(1, std::min<long long>(ceil_div(n, block), 1ll << 30));
 }
 
+// Row partition (multi-GPU): this engine owns global neurons [lo, hi); the
+// edges into them come from every source, and sources are renumbered into the
+// exchange space where rank r's chunk starts at bit r * (nl + 128).
+struct ShardInput {
+    int world = 1, rank = 0;
+    long long q_global = 0, nl = 0, lo = 0, hi = 0;
+    std::vector<uint32_t> soff, sdst;  // global out-adjacency
+    uint32_t xpos(uint32_t src) const {
+        return (uint32_t)((src / nl) * (nl + 128) + src % nl);
+    }
+};
+
 // Tiled-pull layout (see tiled_step_kernel): destinations are cut into
 // tiles of T; each tile's in-edges, visited in ascending source order (the
 // CSR out-adjacency is source-major, so a stable bucket pass keeps that
 // order), are packed into 256-edge segments whose sources span < 2^17.
-int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff,
-                const std::vector<uint32_t>& sdst, const std::vector<uint32_t>& roff_h,
-                std::vector<uint32_t>& heavy) {
+int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff_in,
+                const std::vector<uint32_t>& sdst_in, const std::vector<uint32_t>& roff_h,
+                std::vector<uint32_t>& heavy, const ShardInput* sh) {
+    const std::vector<uint32_t>& soff = sh ? sh->soff : soff_in;
+    const std::vector<uint32_t>& sdst = sh ? sh->sdst : sdst_in;
+    const long long lo = sh ? sh->lo : 0, hi = sh ? sh->hi : e->q;
+    const long long n_src = sh ? sh->q_global : e->q;
     const long long q = e->q;
     DevSys& s = e->sys;
     int n_sm = 148;
@@ -174,21 +193,25 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     const long long n_tiles = std::max<long long>(1, ceil_div(q, T));
     s.tile = (int)T;
     s.n_tiles = n_tiles;
-    // bucket the edges by destination tile (source order preserved)
-    const long long S = (long long)sdst.size();
+    // bucket the edges into local destination tiles (source order preserved)
     std::vector<unsigned long long> start(n_tiles + 1, 0);
-    for (long long e2 = 0; e2 < S; ++e2) start[sdst[e2] / T + 1]++;
+    for (size_t e2 = 0; e2 < sdst.size(); ++e2)
+        if ((long long)sdst[e2] >= lo && (long long)sdst[e2] < hi) start[(sdst[e2] - lo) / T + 1]++;
     for (long long t = 0; t < n_tiles; ++t) start[t + 1] += start[t];
+    const long long S = (long long)start[n_tiles];
     std::vector<unsigned long long> cur(start.begin(), start.end() - 1);
     std::vector<uint32_t> bsrc(S);
     std::vector<uint16_t> bslot(S);
-    for (long long i = 0; i < q; ++i)
+    for (long long i = 0; i < n_src; ++i) {
+        const uint32_t xs = sh ? sh->xpos((uint32_t)i) : (uint32_t)i;
         for (uint32_t e2 = soff[i]; e2 < soff[i + 1]; ++e2) {
-            const uint32_t dst = sdst[e2];
-            const unsigned long long pos = cur[dst / T]++;
-            bsrc[pos] = (uint32_t)i;
-            bslot[pos] = (uint16_t)(dst % T);
+            const long long dst = sdst[e2];
+            if (dst < lo || dst >= hi) continue;
+            const unsigned long long pos = cur[(dst - lo) / T]++;
+            bsrc[pos] = xs;
+            bslot[pos] = (uint16_t)((dst - lo) % T);
         }
+    }
     // segments
     std::vector<uint32_t> tseg(n_tiles + 1, 0), base, last;
     std::vector<uint32_t> words;
@@ -287,7 +310,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
 // Build every device structure.  Host-side work is O(q + m + S) with plain
 // loops; the quadratic layouts (ELL pairs, dense rows) and the in-adjacency
 // transpose are built on the device.
-int build(snp_engine* e, const snp_system_desc* d) {
+int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullptr) {
     const long long q = d->q, m = d->m;
     if (q < 0 || m < 0) return fail(SNP_ERR_BAD_ARG, "q and m must be >= 0");
     if (q >= kInt32Max) return fail(SNP_ERR_CAPACITY, "q=%lld exceeds the int32 neuron index range", q);
@@ -376,8 +399,15 @@ int build(snp_engine* e, const snp_system_desc* d) {
 
     const bool ell_from_matrix = e->format == SNP_FMT_ELL && !have_adj;
     const bool dense_from_matrix = e->format == SNP_FMT_SPARSE && !have_adj;
-    if (e->format == SNP_FMT_COMPRESSED && !have_adj && q > 0)
+    if (sh) {
+        // local out-degrees (traffic counters) from the global adjacency
+        for (long long i = 0; i < q; ++i) {
+            outdeg[i] = sh->soff[sh->lo + i + 1] - sh->soff[sh->lo + i];
+            z = std::max<int>(z, (int)outdeg[i]);
+        }
+    } else if (e->format == SNP_FMT_COMPRESSED && !have_adj && q > 0) {
         return fail(SNP_ERR_BAD_ARG, "COMPRESSED needs adj_offsets/adj_targets or syn_target");
+    }
     if (ell_from_matrix && m > 0 && !(d->ell_target && d->ell_amount))
         return fail(SNP_ERR_BAD_ARG, "ELL needs adj_offsets/adj_targets or ell_target/ell_amount");
     if (dense_from_matrix && m > 0 && q > 0 && !d->sparse_data)
@@ -429,7 +459,8 @@ int build(snp_engine* e, const snp_system_desc* d) {
     }
 
     CU(cudaSetDevice(e->device));
-    CU(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+    e->stream = e->own_stream;
     CU(cudaEventCreate(&e->ev0));
     CU(cudaEventCreate(&e->ev1));
 
@@ -516,7 +547,9 @@ int build(snp_engine* e, const snp_system_desc* d) {
         const bool many_in = e->kind == RECV_PULL && !e->tiled && ((indeg[i] + 3u) & ~3u) > kLightIn;
         if (many_rules || many_in) heavy.push_back((uint32_t)i);
     }
-    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, roff, heavy));
+    if (sh && !(e->tiled && e->p_mode == P_BIT))
+        return fail(SNP_ERR_BAD_ARG, "row partition needs COMPRESSED/tiled and one common produced amount (P bits)");
+    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, roff, heavy, sh));
     uint32_t* d_heavy;
     TRY(upload(e, &d_heavy, heavy));
     s.heavy = d_heavy;
@@ -578,10 +611,18 @@ int build(snp_engine* e, const snp_system_desc* d) {
     TRY(e->alloc(&st.cfg, q + 8));  // +8: 16-byte bulk-copy tails
     TRY(e->alloc(&st.ds, q + 8));
     TRY(e->alloc(&st.chosen, q));
+    if (sh) {
+        s.x_stride = sh->nl / 32 + 4;
+        s.world = sh->world;
+        s.rank = sh->rank;
+        s.gbase = sh->lo;
+        s.xbase = (long long)sh->rank * s.x_stride * 32;
+        e->p_words = s.x_stride * sh->world + 8;
+    }
     if (e->kind == RECV_PULL) {
         long long words;
         switch (e->p_mode) {
-            case P_BIT: words = ceil_div(q + 1, 32) + 8; break;  // +8: bulk-copy tails
+            case P_BIT: words = sh ? e->p_words : ceil_div(q + 1, 32) + 8; break;  // +8: bulk-copy tails
             case P_U8: words = ceil_div(q + 1, 4) + 1; break;
             case P_U16: words = ceil_div(q + 1, 2) + 1; break;
             default: words = q + 2; break;
@@ -686,7 +727,7 @@ int reset_state(snp_engine* e) {
         for (int i = 0; i < 3; ++i) {
             size_t bytes;
             switch (e->p_mode) {
-                case P_BIT: bytes = (ceil_div(q + 1, 32) + 8) * 4; break;
+                case P_BIT: bytes = (e->p_words ? e->p_words : ceil_div(q + 1, 32) + 8) * 4; break;
                 case P_U8: bytes = (ceil_div(q + 1, 4) + 1) * 4; break;
                 case P_U16: bytes = (ceil_div(q + 1, 2) + 1) * 4; break;
                 default: bytes = (q + 2) * 4; break;
@@ -793,7 +834,46 @@ int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
         return fail(SNP_ERR_CUDA, "no CUDA device %d visible (the B200 engine has no CPU fallback)", desc->device);
     auto e = std::make_unique<snp_engine>();
     e->device = desc->device;
-    int rc = build(e.get(), desc);
+    int rc;
+    if (desc->world > 1) {
+        // row partition: build the local slice of the global system
+        const long long q = desc->q;
+        if (desc->rank < 0 || desc->rank >= desc->world) return fail(SNP_ERR_BAD_ARG, "rank out of range");
+        if (desc->format != SNP_FMT_COMPRESSED || !desc->adj_offsets)
+            return fail(SNP_ERR_BAD_ARG, "row partition needs COMPRESSED with adj_offsets/adj_targets");
+        ShardInput sh;
+        sh.world = desc->world;
+        sh.rank = desc->rank;
+        sh.q_global = q;
+        sh.nl = (ceil_div(std::max<long long>(q, 1), desc->world) + 127) / 128 * 128;
+        sh.lo = std::min<long long>(q, (long long)desc->rank * sh.nl);
+        sh.hi = std::min<long long>(q, sh.lo + sh.nl);
+        const long long S = q > 0 ? desc->adj_offsets[q] : 0;
+        if (S >= (1ll << 32) - 1 || (long long)desc->world * (sh.nl + 128) >= (1ll << 32))
+            return fail(SNP_ERR_CAPACITY, "row partition exceeds 32-bit exchange positions");
+        sh.soff.resize(q + 1);
+        sh.sdst.resize(S);
+        for (long long i = 0; i <= q; ++i) sh.soff[i] = (uint32_t)desc->adj_offsets[i];
+        for (long long x = 0; x < S; ++x) {
+            const long long t = desc->adj_targets[x];
+            if (t < 0 || t >= q) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", t);
+            sh.sdst[x] = (uint32_t)t;
+        }
+        // node arrays (initial, offsets, rules) describe this rank's neurons
+        // [lo, hi) only; `m` counts their rules
+        snp_system_desc ld = *desc;
+        ld.q = sh.hi - sh.lo;
+        ld.adj_offsets = nullptr;
+        ld.adj_targets = nullptr;
+        ld.syn_target = nullptr;
+        ld.variant = SNP_VARIANT_TILED;
+        e->shard_lo = sh.lo;
+        e->shard_hi = sh.hi;
+        e->shard_nl = sh.nl;
+        rc = build(e.get(), &ld, &sh);
+    } else {
+        rc = build(e.get(), desc);
+    }
     if (rc != SNP_OK) return rc;
     *out = e.release();
     return SNP_OK;
@@ -839,6 +919,7 @@ int snp_advance(snp_engine* e, const snp_run_opts* o, int64_t n_steps, snp_trace
     if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
     TRY(validate_opts(o));
     if (!e->begun) return fail(SNP_ERR_BAD_ARG, "snp_advance before snp_begin");
+    if (e->sys.x_stride) return fail(SNP_ERR_BAD_ARG, "a row-partitioned engine steps with snp_launch_step + an exchange");
     CU(cudaSetDevice(e->device));
     const long long q = e->q;
     const int record = tr ? o->record : 0;
@@ -1145,6 +1226,65 @@ int snp_update_delays(snp_engine* e, const int64_t* delays, const int64_t* chose
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(next_delays, e->scratch[2], q * 8, cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
+    return SNP_OK;
+}
+
+// --------------------------------------------------------------- row partition
+
+int snp_exchange_info(const snp_engine* e, snp_exchange* x) {
+    if (!e || !x) return fail(SNP_ERR_BAD_ARG, "null argument");
+    memset(x, 0, sizeof(*x));
+    for (int i = 0; i < 3; ++i) x->slot[i] = e->st.P[i];
+    x->world = std::max(1, e->sys.world);
+    x->rank = e->sys.rank;
+    x->lo = e->shard_lo;
+    x->hi = e->sys.x_stride ? e->shard_hi : e->q;
+    x->chunk_bytes = e->sys.x_stride * 4;
+    x->chunk_offset_bytes = (long long)e->sys.rank * e->sys.x_stride * 4;
+    x->slot_bytes = e->sys.x_stride * 4 * x->world;
+    x->neurons_per_rank = e->shard_nl;
+    return SNP_OK;
+}
+
+int snp_set_stream(snp_engine* e, void* stream) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    e->stream = stream ? static_cast<cudaStream_t>(stream) : e->own_stream;
+    return SNP_OK;
+}
+
+int snp_configure(snp_engine* e, const snp_run_opts* o) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    TRY(validate_opts(o));
+    if (!e->begun) return fail(SNP_ERR_BAD_ARG, "snp_configure before snp_begin");
+    CU(cudaSetDevice(e->device));
+    Ctrl& c = e->hctrl;
+    c.max_steps = o->max_steps;
+    c.policy = o->policy;
+    c.seed = o->seed;
+    c.record = 0;
+    c.stats_on = o->collect_stats ? 1 : 0;
+    c.stop_at = 0x3fffffffffffffffll;
+    c.trace_base = 0;
+    TRY(push_ctrl(e));
+    CU(cudaStreamSynchronize(e->stream));
+    return SNP_OK;
+}
+
+int snp_launch_step(snp_engine* e) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    CU(cudaSetDevice(e->device));
+    launch_step(e);
+    CU(cudaGetLastError());
+    return SNP_OK;
+}
+
+int snp_poll(snp_engine* e, snp_result* res) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    CU(cudaSetDevice(e->device));
+    TRY(pull_ctrl(e));
+    fill_result(e, res);
+    if (e->hctrl.halted && e->hctrl.reason == HALT_NEGATIVE)
+        return fail(SNP_ERR_NEGATIVE, "spike counts went negative (row-partitioned run)");
     return SNP_OK;
 }
 

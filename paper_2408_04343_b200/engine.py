@@ -173,7 +173,8 @@ class DeviceEngine:
     def __init__(self, fmt: Format, q: int, rules: RuleVector, offsets: np.ndarray,
                  initial: np.ndarray | None = None, *, adj: tuple[np.ndarray, np.ndarray] | None = None,
                  syn: SynapseMatrix | None = None, ell: EllMatrix | None = None,
-                 sparse: SparseMatrix | None = None, variant: str = "auto", device: int = 0):
+                 sparse: SparseMatrix | None = None, variant: str = "auto", device: int = 0,
+                 world: int = 1, rank: int = 0):
         if fmt not in _FMT_CODES:
             raise ValueError(f"no device backend for format {fmt!r}")
         if variant not in _VARIANTS:
@@ -213,6 +214,7 @@ class DeviceEngine:
             keep["sparse"] = _c64(sparse.data)
             d.sparse_data = nat.i64p(keep["sparse"])
         d.device = device
+        d.world, d.rank = int(world), int(rank)
         handle = nat.ctypes.c_void_p()
         rc = lib.snp_engine_create(nat.ctypes.byref(d), nat.ctypes.byref(handle))
         if rc == nat.SNP_ERR_BAD_ARG:
@@ -225,6 +227,7 @@ class DeviceEngine:
         info = nat.EngineInfo()
         nat.check(lib.snp_engine_get_info(self._h, nat.ctypes.byref(info)))
         self.info = {name: getattr(info, name) for name, _ in nat.EngineInfo._fields_}
+        self.q = int(info.q)  # a row-partitioned engine holds only its own rows
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -325,6 +328,42 @@ class DeviceEngine:
         if rc:
             self._raise(rc, res)
         return total.value, (kern.value if per_kernel else float("nan")), res
+
+    # -- externally exchanged stepping (row partition, sharded.py) ------------------
+
+    def exchange_info(self) -> nat.Exchange:
+        x = nat.Exchange()
+        nat.check(self._lib.snp_exchange_info(self._h, nat.ctypes.byref(x)))
+        return x
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        nat.check(self._lib.snp_set_stream(self._h, nat.ctypes.c_void_p(stream_ptr or 0)))
+
+    def configure(self, max_steps: int, selection: Selection, collect_stats: bool = False) -> None:
+        opts = self._opts(max_steps, selection, collect_stats=collect_stats)
+        rc = self._lib.snp_configure(self._h, nat.ctypes.byref(opts))
+        if rc:
+            self._raise(rc)
+
+    def launch_step(self) -> None:
+        rc = self._lib.snp_launch_step(self._h)
+        if rc:
+            self._raise(rc)
+
+    def poll(self) -> nat.Result:
+        res = nat.Result()
+        rc = self._lib.snp_poll(self._h, nat.ctypes.byref(res))
+        if rc:
+            self._raise(rc, res)
+        return res
+
+    def read_state(self) -> tuple[np.ndarray, np.ndarray]:
+        cfg = np.empty(self.q, dtype=np.int64)
+        dly = np.empty(self.q, dtype=np.int64)
+        rc = self._lib.snp_read_state(self._h, nat.ptr(cfg), nat.ptr(dly))
+        if rc:
+            self._raise(rc)
+        return cfg, dly
 
     # -- phase functions ----------------------------------------------------------
 

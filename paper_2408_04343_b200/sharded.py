@@ -1,0 +1,273 @@
+"""Row-partitioned multi-GPU stepping.
+
+One process per GPU.  Rank r owns neurons [lo_r, hi_r) (``shard_layout``):
+their configuration, delay state, rules and every in-edge entering them
+(sources anywhere).  Per step each rank runs the tiled step kernel on its
+rows, which publishes its production bits P_k and its step flags (fired /
+closed / negative) into its chunk of exchange slot ``k % 3``; an in-place
+all-gather of that slot (NCCL over NVLink under torchrun) makes every rank's
+P_k and flags visible everywhere before step k+1, whose kernel takes the
+halting decision for step k from the gathered flags -- identically on every
+rank, with no host round trip.
+
+Exchange space: rank r's chunk starts at bit r * (nl + 128); its first nl bits
+are its neurons' P bits, the last 4 words its flags.  Sources in the tiled
+in-edge segments are renumbered into this space when the engine is built.
+
+Selection hashes on the global neuron id, so a sharded run is bit-identical
+to the single-engine run (tests/test_sharded.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .engine import DeviceEngine, HaltReason
+from .generators import SYNTH_DEGREE, SYNTH_SEED, SystemArrays
+from .matrices import Format, NeuronRuleMap, RuleVector
+from .selection import FirstApplicable, Selection, mix64_array
+from . import _native as nat
+
+HDR_BITS = 128
+
+
+@dataclass(frozen=True)
+class ShardLayout:
+    q: int
+    world: int
+    nl: int                 # neurons per rank (multiple of 128)
+
+    def bounds(self, rank: int) -> tuple[int, int]:
+        lo = min(self.q, rank * self.nl)
+        return lo, min(self.q, lo + self.nl)
+
+    @property
+    def chunk_words(self) -> int:
+        return self.nl // 32 + HDR_BITS // 32
+
+    def xpos(self, src: np.ndarray) -> np.ndarray:
+        """Exchange-space bit position of global source ids."""
+        src = np.asarray(src, dtype=np.int64)
+        return (src // self.nl) * (self.nl + HDR_BITS) + src % self.nl
+
+    def header_word(self, rank: int) -> int:
+        return rank * self.chunk_words + self.chunk_words - 4
+
+
+def shard_layout(q: int, world: int) -> ShardLayout:
+    """The partition rule of snp_engine_create (include/snpb200.h)."""
+    per = -(-max(q, 1) // world)
+    return ShardLayout(q, world, -(-per // 128) * 128)
+
+
+def decide_halt(flags: np.ndarray) -> HaltReason | str | None:
+    """Halting decision from the gathered per-rank flags [world, 3]
+    (fired, closed, negative) -- the rule the step kernel applies."""
+    f, c, n = (bool(x) for x in np.asarray(flags).any(axis=0))
+    if n:
+        return "negative"
+    if not f and not c:
+        return HaltReason.NO_APPLICABLE_RULES
+    return None
+
+
+def local_arrays(arrays: SystemArrays, layout: ShardLayout, rank: int) -> SystemArrays:
+    """Slice a whole-system SystemArrays to rank ``rank``'s node arrays (the
+    adjacency stays global: the engine keeps the edges entering its rows)."""
+    lo, hi = layout.bounds(rank)
+    off = arrays.rule_map.offsets
+    r0, r1 = int(off[lo]), int(off[hi])
+    r = arrays.rules
+    rules = RuleVector(r.threshold[r0:r1], r.is_exact[r0:r1], r.consumed[r0:r1], r.produced[r0:r1],
+                       r.delay[r0:r1], r.neuron[r0:r1] - lo)
+    return SystemArrays(arrays.initial[lo:hi], rules, NeuronRuleMap(off[lo:hi + 1] - r0),
+                        arrays.adj_offsets, arrays.adj_targets)
+
+
+class _DeviceView:
+    """__cuda_array_interface__ over engine-owned device memory (for torch)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class ShardedEngine:
+    """One rank's engine over its rows of a q-neuron system.
+
+    ``local`` holds the rank's node arrays (``local_arrays`` or
+    ``synth_v1_rows``) and a CSR over all q sources containing (at least)
+    every edge that enters the rank's rows.
+    """
+
+    def __init__(self, local: SystemArrays, q: int, rank: int, world: int, device: int = 0):
+        self.layout = shard_layout(q, world)
+        self.rank, self.world = rank, world
+        self.lo, self.hi = self.layout.bounds(rank)
+        if local.neuron_count != self.hi - self.lo:
+            raise ValueError(f"rank {rank} owns {self.hi - self.lo} neurons, got {local.neuron_count}")
+        self.engine = DeviceEngine(Format.COMPRESSED, q, local.rules, local.rule_map.offsets, local.initial,
+                                   adj=(local.adj_offsets, local.adj_targets), variant="tiled",
+                                   device=device, world=world, rank=rank)
+        self.x = self.engine.exchange_info()
+        self._views = None
+
+    def slots_torch(self):
+        """Torch uint8 views of the three exchange slots and of this rank's
+        chunk in each (for in-place all_gather_into_tensor)."""
+        if self._views is None:
+            import torch
+            full = [torch.as_tensor(_DeviceView(int(self.x.slot[i]), int(self.x.slot_bytes)), device="cuda")
+                    for i in range(3)]
+            lo = int(self.x.chunk_offset_bytes)
+            chunk = [f[lo:lo + int(self.x.chunk_bytes)] for f in full]
+            self._views = (full, chunk)
+        return self._views
+
+    def run(self, max_steps: int, exchange: Callable[[int], None], selection: Selection = FirstApplicable(),
+            poll_every: int = 8, collect_stats: bool = False):
+        """Step to halt.  ``exchange(slot)`` must all-gather exchange slot
+        ``slot`` across ranks after each launch (same call on every rank)."""
+        eng = self.engine
+        eng.begin()
+        eng.configure(max_steps, selection, collect_stats)
+        k = 0
+        while True:
+            eng.launch_step()
+            exchange(k % 3)
+            k += 1
+            if k % poll_every == 0 or k > max_steps:
+                res = eng.poll()
+                if res.halt != nat.SNP_RUNNING:
+                    break
+        cfg, dly = eng.read_state()
+        reason = HaltReason.STEP_LIMIT if res.halt == nat.SNP_HALT_STEP_LIMIT else HaltReason.NO_APPLICABLE_RULES
+        return cfg, dly, int(res.steps), reason, res.stats_dict(), k
+
+
+def torch_allgather_exchange(sh: ShardedEngine, group=None) -> Callable[[int], None]:
+    """Exchange callable over torch.distributed (NCCL under torchrun); the
+    engine launches on torch's current stream so the collective is ordered
+    after the step kernel without a host sync."""
+    import torch
+    import torch.distributed as dist
+    sh.engine.set_stream(torch.cuda.current_stream().cuda_stream)
+    full, chunk = sh.slots_torch()
+
+    def exchange(slot: int) -> None:
+        dist.all_gather_into_tensor(full[slot], chunk[slot], group=group)
+
+    return exchange
+
+
+# -- per-rank synthetic generation (weak-scaling bench) ------------------------------
+
+def synth_v1_rows(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_delays: bool = False,
+                  chunk: int = 4_000_000) -> SystemArrays:
+    """Rows [lo, hi) of ``synth_v1(q)`` plus every edge entering them, without
+    materialising the whole system (counter-based: any rank rebuilds its part)."""
+    idx = np.arange(lo, hi, dtype=np.int64)
+    n = hi - lo
+
+    def h(stream: int, ids: np.ndarray) -> np.ndarray:
+        return mix64_array(seed, stream, ids)
+
+    init = (h(0, idx) % np.uint64(8)).astype(np.int64)
+    t0 = 2 + (h(17, idx) % np.uint64(4)).astype(np.int64)
+    t1 = 3 + (h(18, idx) % np.uint64(6)).astype(np.int64)
+    c1 = 1 + (h(19, idx) % t1.astype(np.uint64)).astype(np.int64)
+    t2 = 1 + (h(20, idx) % np.uint64(5)).astype(np.int64)
+    thr = np.stack([t0, t1, t2, np.ones(n, np.int64)], axis=1)
+    cons = np.stack([t0, c1, t2, np.ones(n, np.int64)], axis=1)
+    prod = np.tile(np.array([1, 1, 0, 1], dtype=np.int64), (n, 1))
+    exact = np.tile(np.array([True, False, True, False]), (n, 1))
+    dly = np.zeros((n, 4), dtype=np.int64)
+    if with_delays:
+        for r, stream in ((0, 21), (1, 22), (3, 23)):
+            dly[:, r] = (h(stream, idx) % np.uint64(4)).astype(np.int64)
+    m = 4 * n
+    rules = RuleVector(thr.reshape(m), exact.reshape(m), cons.reshape(m), prod.reshape(m), dly.reshape(m),
+                       np.repeat(np.arange(n, dtype=np.int64), 4))
+    # edges entering [lo, hi), from every source, as a CSR over all q sources
+    width = (q - 1) // SYNTH_DEGREE
+    srcs, dsts = [], []
+    for a in range(0, q, chunk):
+        ids = np.arange(a, min(q, a + chunk), dtype=np.int64)
+        for k in range(SYNTH_DEGREE):
+            t = (ids + 1 + k * width + (h(1 + k, ids) % np.uint64(width)).astype(np.int64)) % q
+            keep = (t >= lo) & (t < hi)
+            srcs.append(ids[keep])
+            dsts.append(t[keep])
+    src = np.concatenate(srcs) if srcs else np.zeros(0, np.int64)
+    dst = np.concatenate(dsts) if dsts else np.zeros(0, np.int64)
+    order = np.lexsort((dst, src))
+    src, dst = src[order], dst[order]
+    adj_off = np.zeros(q + 1, dtype=np.int64)
+    np.cumsum(np.bincount(src, minlength=q), out=adj_off[1:])
+    return SystemArrays(init, rules, NeuronRuleMap(np.arange(0, m + 1, 4, dtype=np.int64)), adj_off, dst)
+
+
+# -- bench entry (torchrun, N > 1) ------------------------------------------------------
+
+def bench_sharded(args, rank: int, world: int) -> None:
+    """Weak scaling: q = world x 10^7, each rank owns 10^7 rows; value is
+    whole-job 10^7-neuron-steps/s (= world x system steps/s)."""
+    import json
+    import os
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    q = args.q * world
+    layout = shard_layout(q, world)
+    lo, hi = layout.bounds(rank)
+    t0 = time.perf_counter()
+    local = synth_v1_rows(q, lo, hi, with_delays=(args.workload == "k4"))
+    gen_s = time.perf_counter() - t0
+    sh = ShardedEngine(local, q, rank, world, device=local_rank)
+    ex = torch_allgather_exchange(sh)
+    sel = FirstApplicable()
+    eng = sh.engine
+    eng.begin()
+    eng.configure(1 << 62, sel)
+    k = 0
+    for _ in range(args.warmup):
+        eng.launch_step()
+        ex(k % 3)
+        k += 1
+    torch.cuda.synchronize()
+    dist.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(args.steps):
+        eng.launch_step()
+        ex(k % 3)
+        k += 1
+    stop.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([start.elapsed_time(stop)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    res = eng.poll()
+    if rank == 0:
+        ms_step = ms.item() / args.steps
+        line = {
+            "metric": "SNP steps/sec at 10^7 neurons", "value": world * 1000.0 / ms_step, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (synth-v1 rows per rank)",
+            "config": {"workload": f"synth-v1 q={q} ({world} x 10^7), row-partitioned, NCCL all-gather of P bits",
+                       "format": "compressed", "variant": "tiled", "policy": "first",
+                       "parallelism": f"rows/{world}", "exchange_bytes_per_step": int(sh.x.slot_bytes)},
+            "system_steps_per_s": 1000.0 / ms_step, "gpu_launches": args.steps, "halt": int(res.halt),
+            "setup_s": {"generate": gen_s},
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), f"{name} missing from {nat.LIB_PATH}"
     assert {n for n, _, _ in nat.SIGNATURES} == set(names)
-    assert lib.snp_abi_version() == 1
+    assert lib.snp_abi_version() == 2
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -39,8 +39,8 @@ def test_struct_layouts_match_header(tmp_path):
 #include <stddef.h>
 #include "{HEADER}"
 int main(void) {{
-  printf("%zu %zu %zu %zu %zu\\n", sizeof(snp_system_desc), sizeof(snp_run_opts),
-         sizeof(snp_trace_out), sizeof(snp_result), sizeof(snp_engine_info));
+  printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(snp_system_desc), sizeof(snp_run_opts),
+         sizeof(snp_trace_out), sizeof(snp_result), sizeof(snp_engine_info), sizeof(snp_exchange));
   printf("%zu %zu %zu\\n", offsetof(snp_system_desc, sparse_data), offsetof(snp_result, stats),
          offsetof(snp_run_opts, collect_stats));
   return 0;
@@ -49,7 +49,8 @@ int main(void) {{
     exe = tmp_path / "probe"
     subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(src)], check=True)
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
-    sizes = [ctypes.sizeof(c) for c in (nat.SystemDesc, nat.RunOpts, nat.TraceOut, nat.Result, nat.EngineInfo)]
+    sizes = [ctypes.sizeof(c) for c in (nat.SystemDesc, nat.RunOpts, nat.TraceOut, nat.Result, nat.EngineInfo,
+                                        nat.Exchange)]
     offs = [nat.SystemDesc.sparse_data.offset, nat.Result.stats.offset, nat.RunOpts.collect_stats.offset]
     assert [int(x) for x in out] == sizes + offs
 

@@ -1,0 +1,201 @@
+"""Row partition (multi-GPU path, paper_2408_04343_b200/sharded.py).
+
+CPU: the exchange protocol -- partition rule, exchange-space renumbering,
+per-rank flags, halting agreement -- run by 2 gloo processes with a numpy
+emulation of each rank's step, against the unsharded oracle.
+GPU: 2 and 3 row-partitioned engines on one B200 with an emulated all-gather,
+bit-identical to the single engine.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2408_04343_b200 as snp
+from paper_2408_04343_b200 import sharded as shd
+from conftest import corpus_system
+from oracle import coracle
+from oracle.snp_oracle import OracleSystem
+
+
+# -- partition rule ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("q,world", [(1, 2), (1000, 3), (10**7, 8), (12288, 8), (129, 2)])
+def test_layout_covers_all_rows(q, world):
+    L = shd.shard_layout(q, world)
+    assert L.nl % 128 == 0
+    bounds = [L.bounds(r) for r in range(world)]
+    assert bounds[0][0] == 0 and bounds[-1][1] == q
+    for (a, b), (c, d) in zip(bounds, bounds[1:]):
+        assert b == c and a <= b
+    src = np.arange(q)
+    x = L.xpos(src)
+    assert (np.diff(x) > 0).all()                       # order preserved (sorted segments stay sorted)
+    assert ((x % (L.nl + 128)) < L.nl).all()            # never lands in a header
+
+
+def test_decide_halt_rule():
+    assert shd.decide_halt(np.array([[0, 0, 0], [0, 0, 0]])) is snp.HaltReason.NO_APPLICABLE_RULES
+    assert shd.decide_halt(np.array([[0, 1, 0], [0, 0, 0]])) is None
+    assert shd.decide_halt(np.array([[1, 0, 0], [0, 0, 0]])) is None
+    assert shd.decide_halt(np.array([[1, 0, 0], [0, 0, 1]])) == "negative"
+
+
+# -- protocol over gloo (CPU) ----------------------------------------------------------------
+
+def _emulated_rank_step(osys, L, rank, cfg, dsv, pbits_full, k, max_steps):
+    """One rank's step, as the tiled kernel does it: finish step k-1 from the
+    gathered P bits, then select step k.  Returns (cfg, dsv, P chunk bits, flags)."""
+    lo, hi = L.bounds(rank)
+    n = hi - lo
+    src = np.repeat(np.arange(osys.q), np.diff(osys.adj_offsets))
+    dst = osys.adj_targets
+    keep = (dst >= lo) & (dst < hi)
+    xs = L.xpos(src[keep])
+    got = np.zeros(n, dtype=np.int64)
+    np.add.at(got, dst[keep] - lo, pbits_full[xs])
+    open_prev = dsv <= 0
+    C = cfg + np.where(open_prev, got * int(osys.produced[osys.produced > 0][0]), 0)
+    D = np.where(dsv < 0, -dsv - 1, np.maximum(dsv - 1, 0))
+    neg = bool((C < 0).any())
+    bits = np.zeros(n, dtype=np.int64)
+    fired = closed = False
+    new_cfg, new_ds = C.copy(), D.copy()
+    if k < max_steps:
+        for j in range(n):
+            closed |= D[j] != 0
+            if D[j] != 0:
+                continue
+            g = lo + j
+            ok = [r for r in range(osys.offsets[g], osys.offsets[g + 1])
+                  if (C[j] == osys.threshold[r] if osys.is_exact[r] else C[j] >= osys.threshold[r])]
+            if ok:
+                r = ok[0]
+                fired = True
+                new_cfg[j] = C[j] - osys.consumed[r]
+                new_ds[j] = -(osys.delay[r] + 1)
+                bits[j] = 1 if osys.produced[r] > 0 else 0
+    return new_cfg, new_ds, bits, np.array([fired, closed, neg], dtype=np.int64)
+
+
+def _gloo_worker(rank, world, port, q_case, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    osys = OracleSystem.from_arrays(snp.synth_v1(q_case, with_delays=True))
+    L = shd.shard_layout(osys.q, world)
+    lo, hi = L.bounds(rank)
+    cfg = osys.initial[lo:hi].copy()
+    dsv = np.zeros(hi - lo, dtype=np.int64)
+    width = world * (L.nl + 128)
+    pbits = np.zeros(width, dtype=np.int64)
+    max_steps, k = 12, 0
+    while True:
+        if k > 0:
+            flags = pbits_flags
+            if shd.decide_halt(flags) is not None:
+                halt = shd.decide_halt(flags)
+                break
+        cfg, dsv, bits, flags_local = _emulated_rank_step(osys, L, rank, cfg, dsv, pbits, k, max_steps)
+        if k == max_steps:
+            halt = snp.HaltReason.STEP_LIMIT
+            break
+        chunk = torch.zeros(L.nl + 128, dtype=torch.int64)
+        chunk[:hi - lo] = torch.from_numpy(bits)
+        chunk[L.nl:L.nl + 3] = torch.from_numpy(flags_local)
+        parts = [torch.zeros_like(chunk) for _ in range(world)]
+        dist.all_gather(parts, chunk)
+        full = torch.cat(parts).numpy()
+        pbits = full.copy()
+        pbits_flags = np.stack([p.numpy()[L.nl:L.nl + 3] for p in parts])
+        k += 1
+    gathered = [torch.zeros(L.nl, dtype=torch.int64) for _ in range(world)]
+    mine = torch.zeros(L.nl, dtype=torch.int64)
+    mine[:hi - lo] = torch.from_numpy(cfg)
+    dist.all_gather(gathered, mine)
+    if rank == 0:
+        out.put((np.concatenate([g.numpy() for g in gathered])[:osys.q], k, str(halt)))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2])
+def test_protocol_over_gloo_matches_oracle(world):
+    q = 600
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    final, steps, halt = out.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    osys = OracleSystem.from_arrays(snp.synth_v1(q, with_delays=True))
+    tr, want, _ = coracle.run(osys, 12)
+    np.testing.assert_array_equal(final, want)
+    assert steps == tr.n_steps
+
+
+# -- GPU: row-partitioned engines, emulated all-gather ---------------------------------------
+
+def _run_sharded_on_one_gpu(arrays, world, max_steps, selection=snp.FirstApplicable()):
+    q = arrays.neuron_count
+    L = shd.shard_layout(q, world)
+    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world) for r in range(world)]
+    views = [r.slots_torch() for r in ranks]
+    for r in ranks:
+        r.engine.begin()
+        r.engine.configure(max_steps, selection)
+    k = 0
+    while True:
+        for r in ranks:
+            r.engine.launch_step()
+        torch.cuda.synchronize()
+        slot = k % 3
+        for i, r in enumerate(ranks):          # emulated all-gather of slot k % 3
+            off, nb = int(r.x.chunk_offset_bytes), int(r.x.chunk_bytes)
+            for j, other in enumerate(ranks):
+                if i != j:
+                    views[j][0][slot][off:off + nb].copy_(views[i][1][slot])
+        torch.cuda.synchronize()
+        k += 1
+        res = [r.engine.poll() for r in ranks]
+        halts = {int(x.halt) for x in res}
+        assert len(halts) == 1, "ranks disagree on halting"
+        if res[0].halt != 0:
+            break
+    cfg = np.concatenate([r.engine.read_state()[0] for r in ranks])
+    dly = np.concatenate([r.engine.read_state()[1] for r in ranks])
+    return cfg, dly, int(res[0].steps), int(res[0].halt)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["synth", "synth_delays_seeded", "sort"])
+def test_sharded_engines_match_single(world, case):
+    if case == "sort":
+        arrays = snp.sort_arrays(snp.SortInstance(300))
+        L, sel = 400, snp.FirstApplicable()
+    else:
+        arrays = snp.synth_v1(50_000, with_delays=case != "synth")
+        L = 10
+        sel = snp.SeededRandom(77) if "seeded" in case else snp.FirstApplicable()
+    want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED), snp.SimOptions(max_steps=L, selection=sel))
+    cfg, dly, steps, halt = _run_sharded_on_one_gpu(arrays, world, L, sel)
+    np.testing.assert_array_equal(cfg, want.config)
+    np.testing.assert_array_equal(dly, want.delays)
+    assert steps == want.steps
+    if case == "sort":
+        assert halt == 2 and cfg[600:].tolist() == list(range(1, 301))
