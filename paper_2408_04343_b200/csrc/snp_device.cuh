@@ -55,7 +55,7 @@ static_assert(kTileThreads % 32 == 0 && kTileThreads + 32 <= 1024, "CTA must fit
 constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
 constexpr uint32_t kDstBits = 15;         // destination slot within a tile
 constexpr uint32_t kSrcSpan = 1u << 17;   // source offset range within a segment
-constexpr uint32_t kDummyEdge = 0xffffffffu;
+constexpr uint32_t kDummyEdge = 0xffffffffu;  // CSR / legacy padding marker
 constexpr int kMaxTile = (1 << kDstBits) - 32;
 enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
 enum Rec { REC_CONFIGS = 1, REC_DELAYS = 2, REC_SPIKING = 4 };
@@ -978,28 +978,29 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 for (uint32_t i = warp; i < n; i += kWarpsC) {
                     // lane l takes edges l, l+32, ...: each instruction covers 32
                     // consecutive (source-sorted) edges, so the P-bit loads hit
-                    // nearly consecutive words -- conflict-free shared loads
+                    // nearly consecutive words -- conflict-free shared loads.
+                    // Padding edges are (0, slot T): a real lookup into the
+                    // dummy counter, so the loop has no branches.
                     const uint32_t base = h->bases[i];
+                    const uint32_t rel0 = base - src0;
                     const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf + kPayload + i * kSegEdges * 4u) + lane;
-                    uint32_t w[8], v[8];
+                    uint32_t w[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) w[e] = wp[e * 32];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        const uint32_t src = base + (w[e] >> kDstBits);
-                        if (w[e] == kDummyEdge) {
-                            v[e] = 0u;
-                        } else if (PM == P_BIT) {
-                            const uint32_t rel = src - src0;
-                            v[e] = (ps[rel >> 5] >> (src & 31)) & 1u;
+                        uint32_t v;
+                        if (PM == P_BIT) {
+                            const uint32_t rel = rel0 + (w[e] >> kDstBits);
+                            v = (ps[rel >> 5] >> (rel & 31)) & 1u;  // src0 is a multiple of 128
                         } else {
-                            v[e] = (uint32_t)p_lookup<PM>(Pprev, src);
+                            v = (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits));
                         }
+                        atomicAdd(&acc[w[e] & ((1u << kDstBits) - 1u)], v);
                     }
+                    if (stats_on) {
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        if (v[e]) atomicAdd(&acc[w[e] & ((1u << kDstBits) - 1u)], v[e]);
-                        stat[ST_EDGES] += (w[e] != kDummyEdge) ? 1u : 0u;
+                        for (int e = 0; e < 8; ++e) stat[ST_EDGES] += ((w[e] & ((1u << kDstBits) - 1u)) != (uint32_t)T);
                     }
                 }
                 __syncwarp();

@@ -229,7 +229,8 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
                 ++n;
             }
             last.push_back(bsrc[e2 - 1]);
-            for (; n < kSegEdges; ++n) words.push_back(kDummyEdge);
+            // padding: source offset 0 (inside the window), dummy counter slot T
+            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T);
         }
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
