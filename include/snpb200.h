@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SNPB200_ABI_VERSION 2
+#define SNPB200_ABI_VERSION 3
 
 enum {
     SNP_OK = 0,
@@ -146,6 +146,9 @@ typedef struct snp_engine_info {
     int64_t p_common;
     int64_t tile;             /* tiled: destinations per tile */
     int64_t n_tiles;
+    int32_t ring_stages;      /* tiled: TMA ring stages in shared memory */
+    int32_t counter_bits;     /* tiled: 16 or 32-bit destination counters */
+    int64_t stage_bytes;      /* tiled: bytes per ring stage */
 } snp_engine_info;
 
 int snp_abi_version(void);

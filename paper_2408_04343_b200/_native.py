@@ -77,6 +77,7 @@ class EngineInfo(ctypes.Structure):
         ("p_mode", ctypes.c_int32), ("heavy_neurons", ctypes.c_int32),
         ("in_edges", ctypes.c_int64), ("p_common", ctypes.c_int64),
         ("tile", ctypes.c_int64), ("n_tiles", ctypes.c_int64),
+        ("ring_stages", ctypes.c_int32), ("counter_bits", ctypes.c_int32), ("stage_bytes", ctypes.c_int64),
     ]
 
 

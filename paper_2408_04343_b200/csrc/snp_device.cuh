@@ -123,6 +123,7 @@ struct DevSys {
     const uint32_t* tseg;       // [n_tiles + 1] segment range of each tile
     const uint32_t* theavy;     // [n_tiles + 1] range of s.heavy inside each tile
     int tile;                   // destinations per tile (multiple of 32)
+    int ring;                   // TMA ring stages (<= kMaxRing)
     long long n_tiles;
     // row partition (sharded.py): local neuron j is global neuron gbase + j and
     // publishes its P bit at exchange-space position xbase + j; rank r's chunk
@@ -467,6 +468,49 @@ __device__ __forceinline__ long long light_commit(const DevSys& s, const DevStat
     return pval;
 }
 
+// Lean light-neuron tail (no recording, no counters) for <= 4 compact rule
+// words already in shared memory: the same decisions as light_commit, computed
+// branch-free on a 32-bit saturated count (thresholds are < 2^31).  A negative
+// count selects nothing, as in light_commit (no guard matches C < 0).
+template <int PM>
+__device__ __forceinline__ long long lean_commit4(const DevSys& s, const DevState& st, const StepCtx& cx, long long j,
+                                                  uint32_t nr, const uint2* rp, long long C, int D, bool can_sel,
+                                                  bool& t_fired, bool& t_closed, bool& t_neg, long long& neg_idx,
+                                                  long long& neg_val) {
+    if (C < 0) {
+        t_neg = true;
+        neg_idx = j + s.gbase;
+        neg_val = C;
+    }
+    t_closed |= D != 0;
+    const uint2 w0 = rp[0], w1 = rp[1], w2 = rp[2], w3 = rp[3];
+    const uint32_t cc = (C >> 31) != 0 ? 0x80000000u : (uint32_t)C;
+    auto ok = [cc](uint32_t g) -> uint32_t {
+        const uint32_t t = g & ~kExactBit;
+        return (g & kExactBit) ? (cc == t) : (cc >= t);
+    };
+    uint32_t mask = ok(w0.x) | (ok(w1.x) << 1) | (ok(w2.x) << 2) | (ok(w3.x) << 3);
+    mask &= (can_sel && C >= 0) ? (1u << nr) - 1u : 0u;
+    int idx;
+    if (cx.policy == 0) {
+        idx = __ffs(mask) - 1;
+    } else {
+        idx = mask ? nth_set_bit(mask, (uint32_t)(mix64(cx.seed, cx.k, j + s.gbase) % (uint32_t)__popc(mask))) : 0;
+    }
+    const uint32_t y = idx <= 0 ? w0.y : (idx == 1 ? w1.y : (idx == 2 ? w2.y : w3.y));
+    const bool fired = mask != 0;
+    t_fired |= fired;
+    st.cfg[j] = fired ? C - (long long)(y & 0xffffu) : C;
+    st.ds[j] = fired ? -(int)((y >> 24) + 1u) : D;
+    const uint32_t p = fired ? (y >> 16) & 0xffu : 0u;
+    if (PM != P_BIT && cx.sel) {
+        if (PM == P_U8) reinterpret_cast<uint8_t*>(cx.Pcur)[j + s.xbase] = (uint8_t)p;
+        else if (PM == P_U16) reinterpret_cast<uint16_t*>(cx.Pcur)[j + s.xbase] = (uint16_t)p;
+        else cx.Pcur[j + s.xbase] = p;
+    }
+    return (long long)p;
+}
+
 // ---------------------------------------------------------------------------
 // The fused step kernel.
 //
@@ -792,12 +836,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // each.  The ring spans tiles, so the next tile's first segments are already
 // in flight while phase 3 / phase 2 finish.
 
-#ifndef SNP_RING_STAGES
-#define SNP_RING_STAGES 2
-#endif
-constexpr int kRingStages = SNP_RING_STAGES;
+constexpr int kMaxRing = 8;  // ring stages (runtime s.ring <= kMaxRing, chosen by the host)
 constexpr int kWarpsC = kTileThreads / 32;              // consumer warps
-constexpr uint32_t kStageBytes = 64u * 1024u;           // one ring stage
+#ifndef SNP_STAGE_KB
+#define SNP_STAGE_KB 48
+#endif
+constexpr uint32_t kStageBytes = SNP_STAGE_KB * 1024u;  // one ring stage
 constexpr uint32_t kHdrBytes = 512;                     // stage header (+ segment bases)
 constexpr uint32_t kMaxSegPerStage = (kHdrBytes - 32) / 4;
 constexpr int kSub = kTileThreads;                      // destinations per phase-2 stage
@@ -822,6 +866,11 @@ constexpr uint32_t kPayload = kHdrBytes;
 
 __device__ __forceinline__ uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
 
+// Shared 32-bit words holding the per-destination counters of a tile of T
+// destinations plus the dummy slot T that padding edges accumulate into.
+template <bool A16>
+__host__ __device__ constexpr int acc_words(int T) { return A16 ? (T + 2) / 2 : T + 1; }
+
 // Stage descriptor (built on the host, build_tiles): 32 bytes.
 //   phase 1: {1 | last << 8, first segment, n segments, src0, P bytes, bases offset, 0, 0}
 //   phase 2: {2 | last << 8, first destination, n, r_al, rule bytes (0 = not staged), 0, 0, 0}
@@ -829,13 +878,19 @@ struct StageDesc {
     uint4 a, b;
 };
 
-template <int PM, bool WIDE>
+// A16: per-destination counters are 16-bit halves of 32-bit words (slot i in
+// word i >> 1), chosen by the host when no destination can receive >= 2^16
+// (halves the counter footprint, so the ring gets a deeper pipeline).
+// LEAN: no trace recording and no traffic counters (compiled out; the host
+// launches this instance only for runs with record == 0 and stats off).
+template <int PM, bool WIDE, bool A16, bool LEAN>
 __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys s, DevState st) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* ring = smem;                                                     // kRingStages x kStageBytes
-    uint32_t* acc = reinterpret_cast<uint32_t*>(smem + kRingStages * kStageBytes);  // [tile + 1]
-    __shared__ __align__(8) uint64_t full_bar[kRingStages];
-    __shared__ __align__(8) uint64_t empty_bar[kRingStages];
+    const int nst = s.ring;                                                   // ring stages
+    uint8_t* ring = smem;                                                     // nst x kStageBytes
+    uint32_t* acc = reinterpret_cast<uint32_t*>(smem + nst * kStageBytes);    // [acc_words(tile)]
+    __shared__ __align__(8) uint64_t full_bar[kMaxRing];
+    __shared__ __align__(8) uint64_t empty_bar[kMaxRing];
     __shared__ __align__(16) StageDesc desc_s[32];
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
@@ -870,8 +925,8 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     const bool sel = k < vc->max_steps;
     const int policy = vc->policy;
     const unsigned long long seed = vc->seed;
-    const int record = vc->record;
-    const bool stats_on = vc->stats_on != 0;
+    const int record = LEAN ? 0 : vc->record;
+    const bool stats_on = LEAN ? false : vc->stats_on != 0;
     const long long slot = k - vc->trace_base;
     const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
     uint32_t* Pcur = pick3(st.P, k % 3);
@@ -889,7 +944,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
 
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kRingStages; ++b) {
+        for (int b = 0; b < nst; ++b) {
             mbar_init(&full_bar[b], 1);
             mbar_init(&empty_bar[b], kWarpsC);
         }
@@ -899,7 +954,8 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
 
     if (warp == kWarpsC) {
         // ================= producer warp: descriptors 32 at a time, lane 0 issues the TMA copies
-        uint32_t n_issued = 0;
+        int pb = 0;           // next ring stage to fill
+        uint32_t pround = 0;  // completed passes over the ring
         const uint32_t rw_size = WIDE ? 16u : 8u;
         for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
             const long long d0 = tile * T;
@@ -914,12 +970,15 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    for (uint32_t i = 0; i < cnt; ++i, ++n_issued) {
+                    for (uint32_t i = 0; i < cnt; ++i) {
                         const uint4 da = desc_s[i].a, db = desc_s[i].b;
                         const uint32_t kind = da.x, first = da.y, n = da.z, f3 = da.w, f4 = db.x, f5 = db.y;
-                        const int b = n_issued % kRingStages;
-                        if (n_issued >= (uint32_t)kRingStages)
-                            mbar_wait(&empty_bar[b], ((n_issued / kRingStages) - 1) & 1u);
+                        const int b = pb;
+                        if (pround > 0) mbar_wait(&empty_bar[b], (pround - 1) & 1u);
+                        if (++pb == nst) {
+                            pb = 0;
+                            ++pround;
+                        }
                         fence_proxy_async_smem();
                         uint8_t* buf = ring + b * kStageBytes;
                         StageHdr* h = reinterpret_cast<StageHdr*>(buf);
@@ -959,21 +1018,26 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
         }
     } else {
         // ================= consumer warps
-        uint32_t cons = 0;
+        int cb = 0;           // next ring stage to consume
+        uint32_t cround = 0;  // completed passes over the ring
         for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
             const long long d0 = tile * T;
             const int nd = (int)min((long long)T, q - d0);
-            for (int i = threadIdx.x; i <= T; i += kTileThreads) acc[i] = 0;
+            for (int i = threadIdx.x; i < acc_words<A16>(T); i += kTileThreads) acc[i] = 0;
             consumer_sync(kTileThreads);
 
             // ---- phase 1: receive sums
             for (;;) {
-                const int b = cons % kRingStages;
+                const int b = cb;
                 const uint8_t* buf = ring + b * kStageBytes;
-                mbar_wait(&full_bar[b], (cons / kRingStages) & 1u);
-                ++cons;
+                mbar_wait(&full_bar[b], cround & 1u);
+                if (++cb == nst) {
+                    cb = 0;
+                    ++cround;
+                }
                 const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
                 const uint32_t n = h->n, last = h->last, src0 = h->src0;
+                const bool pst = h->pstaged != 0;
                 const uint32_t* ps = reinterpret_cast<const uint32_t*>(buf + kPayload + n * kSegEdges * 4u);
                 for (uint32_t i = warp; i < n; i += kWarpsC) {
                     // lane l takes edges l, l+32, ...: each instruction covers 32
@@ -987,16 +1051,22 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     uint32_t w[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) w[e] = wp[e * 32];
+                    auto add = [&](uint32_t we, uint32_t v) {
+                        const uint32_t slot = we & ((1u << kDstBits) - 1u);
+                        if (A16) atomicAdd(&acc[slot >> 1], v << ((slot & 1u) << 4));
+                        else atomicAdd(&acc[slot], v);
+                    };
+                    if (PM == P_BIT && pst) {
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        uint32_t v;
-                        if (PM == P_BIT) {
+                        for (int e = 0; e < 8; ++e) {
                             const uint32_t rel = rel0 + (w[e] >> kDstBits);
-                            v = (ps[rel >> 5] >> (rel & 31)) & 1u;  // src0 is a multiple of 128
-                        } else {
-                            v = (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits));
+                            add(w[e], (ps[rel >> 5] >> (rel & 31)) & 1u);  // src0 is a multiple of 128
                         }
-                        atomicAdd(&acc[w[e] & ((1u << kDstBits) - 1u)], v);
+                    } else {
+                        // P looked up in global memory (L1/L2): non-bit P, or
+                        // windows not staged
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) add(w[e], (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits)));
                     }
                     if (stats_on) {
 #pragma unroll
@@ -1011,10 +1081,13 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
 
             // ---- phase 2: finish step k-1, select step k (one destination per thread)
             for (;;) {
-                const int b = cons % kRingStages;
+                const int b = cb;
                 const uint8_t* buf = ring + b * kStageBytes;
-                mbar_wait(&full_bar[b], (cons / kRingStages) & 1u);
-                ++cons;
+                mbar_wait(&full_bar[b], cround & 1u);
+                if (++cb == nst) {
+                    cb = 0;
+                    ++cround;
+                }
                 const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
                 const uint32_t n = h->n, last = h->last, first = h->first, r_al = h->r_al;
                 const bool rstaged = h->rstaged != 0;
@@ -1040,7 +1113,19 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 const bool heavy = active && nr > kLightRules;
                 int r = -1;
                 long long pval = 0;
-                if (active) {
+                if (LEAN && !WIDE && rstaged && __all_sync(0xffffffffu, !active || nr <= 4u)) {
+                    // lean fast path: <= 4 staged rule words per neuron, branch-free selection
+                    if (active) {
+                        long long C = Cprev;
+                        if (ds_open(dsv)) {
+                            const uint32_t gsum = A16 ? (acc[i >> 1] >> ((i & 1) << 4)) & 0xffffu : acc[i];
+                            C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
+                        }
+                        const int D = ds_next(dsv);
+                        pval = lean_commit4<PM>(s, st, cx, j, nr, reinterpret_cast<const uint2*>(rules_s) + (r0 - r_al),
+                                                C, D, sel && D == 0, t_fired, t_closed, t_neg, neg_idx, neg_val);
+                    }
+                } else if (active) {
                     const bool open_prev = ds_open(dsv);
                     const int D = ds_next(dsv);
                     const bool can_sel = sel && D == 0 && !heavy;
@@ -1061,7 +1146,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     }
                     long long C = Cprev;
                     if (open_prev) {
-                        const uint32_t gsum = acc[i];
+                        const uint32_t gsum = A16 ? (acc[i >> 1] >> ((i & 1) << 4)) & 0xffffu : acc[i];
                         C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
                     }
                     pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3,

@@ -70,6 +70,8 @@ struct snp_engine {
     int z = 0;
     int p_mode = P_BIT;
     long long p_common = 1;
+    long long p_max = 0;      // largest produced amount
+    bool acc16 = false;       // tiled: 16-bit destination counters (acc_words)
     long long in_edges = 0;
     int kind = RECV_PULL;
     bool tiled = false;
@@ -87,6 +89,7 @@ struct snp_engine {
     DevSys sys{};
     DevState st{};
     StepFn step_fn = nullptr;
+    StepFn lean_fn = nullptr;  // tiled: instance without recording / counters
     PrimeFn prime_fn = nullptr;
     int step_grid = 0;
     int push_grid = 0;
@@ -98,6 +101,7 @@ struct snp_engine {
     // graph cache
     cudaGraphExec_t graph = nullptr;
     long long graph_iters = 0;
+    StepFn graph_fn = nullptr;
     long long tr_rows = 0;
     // phase scratch
     long long* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -179,16 +183,41 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     heavy.clear();
     for (long long i = 0; i < q; ++i)
         if (d->offsets[i + 1] - d->offsets[i] > (long long)kLightRules) heavy.push_back((uint32_t)i);
+    // 16-bit counters when no destination can receive 2^16 or more per step
+    // (P_BIT counts sending in-neighbours; other modes sum produced amounts)
+    {
+        std::vector<uint32_t> indeg(std::max<long long>(q, 1), 0);
+        for (size_t e2 = 0; e2 < sdst.size(); ++e2)
+            if ((long long)sdst[e2] >= lo && (long long)sdst[e2] < hi) indeg[sdst[e2] - lo]++;
+        const long long unit = e->p_mode == P_BIT ? 1 : std::max<long long>(1, e->p_max);
+        long long worst = 0;
+        for (uint32_t x : indeg) worst = std::max<long long>(worst, (long long)x * unit);
+        e->acc16 = worst < 65536;
+        if (const char* env = getenv("SNPB200_ACC16")) e->acc16 = e->acc16 && atoi(env) != 0;
+    }
     // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
     long long T = ceil_div(std::max<long long>(q, 1), 4ll * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
     if (const char* env = getenv("SNPB200_TILE")) T = atoll(env);
-    // shared memory: the TMA ring plus one 32-bit counter per destination
+    // shared memory: the TMA ring (2..kMaxRing stages) plus the destination
+    // counters; the ring gets what the counters of a T-tile leave, and T only
+    // shrinks when not even two stages would fit
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
-    const long long t_smem = ((long long)smem_optin - (long long)kRingStages * kStageBytes - 1024) / 4 - 1;
-    T = std::min<long long>(std::min<long long>(kMaxTile, t_smem), std::max<long long>(32, (T + 31) / 32 * 32));
+    cudaFuncAttributes fa{};
+    CU(cudaFuncGetAttributes(&fa, tiled_step_kernel<P_BIT, true, false, false>));
+    const long long budget = (long long)smem_optin - (long long)fa.sharedSizeBytes - 128;
+    auto acc_b = [&](long long t) { return 4ll * (e->acc16 ? acc_words<true>((int)t) : acc_words<false>((int)t)); };
+    T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
+    long long ring = std::min<long long>(kMaxRing, (budget - acc_b(T)) / (long long)kStageBytes);
+    if (const char* env = getenv("SNPB200_RING")) ring = std::min<long long>(ring, atoll(env));
+    if (ring < 2) {
+        ring = 2;
+        while (T > 32 && acc_b(T) > budget - 2ll * kStageBytes) T -= 32;
+    }
     T = T / 32 * 32;
+    s.ring = (int)ring;
+    if (acc_b(T) + ring * (long long)kStageBytes > budget) T = 0;
     if (T < 32) return fail(SNP_ERR_CAPACITY, "not enough shared memory for the tiled kernel");
     const long long n_tiles = std::max<long long>(1, ceil_div(q, T));
     s.tile = (int)T;
@@ -241,6 +270,10 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     std::vector<StageDesc> desc;
     std::vector<uint32_t> tstage(n_tiles + 1, 0), sbases;
     const uint32_t rw_size = e->wide_rules ? 16u : 8u;
+    // P_BIT: stage the P-bit window of a stage's sources with its segments
+    // (SNPB200_PSTAGE=0: look the bits up through L1/L2 instead)
+    bool stage_p = e->p_mode == P_BIT;
+    if (const char* env = getenv("SNPB200_PSTAGE")) stage_p = stage_p && atoi(env) != 0;
     auto r16 = [](unsigned long long x) { return (uint32_t)((x + 15) & ~15ull); };
     for (long long t = 0; t < n_tiles; ++t) {
         uint32_t g = tseg[t];
@@ -250,7 +283,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
             if (g < g1) {
                 src0 = base[g] & ~127u;
                 while (g + n < g1 && n < kMaxSegPerStage) {
-                    const uint32_t pb = e->p_mode == P_BIT ? r16((last[g + n] + 1u - src0 + 7u) / 8u) : 0u;
+                    const uint32_t pb = stage_p ? r16((last[g + n] + 1u - src0 + 7u) / 8u) : 0u;
                     if (kPayload + (n + 1) * kSegEdges * 4u + pb > kStageBytes) break;
                     pbytes = pb;
                     ++n;
@@ -311,6 +344,25 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
 // Build every device structure.  Host-side work is O(q + m + S) with plain
 // loops; the quadratic layouts (ELL pairs, dense rows) and the in-adjacency
 // transpose are built on the device.
+template <int PM>
+void pick_tiled(snp_engine* e) {
+    if (e->wide_rules) {
+        e->step_fn = e->acc16 ? tiled_step_kernel<PM, true, true, false> : tiled_step_kernel<PM, true, false, false>;
+        e->lean_fn = e->acc16 ? tiled_step_kernel<PM, true, true, true> : tiled_step_kernel<PM, true, false, true>;
+    } else {
+        e->step_fn = e->acc16 ? tiled_step_kernel<PM, false, true, false> : tiled_step_kernel<PM, false, false, false>;
+        e->lean_fn = e->acc16 ? tiled_step_kernel<PM, false, true, true> : tiled_step_kernel<PM, false, false, true>;
+    }
+    e->prime_fn = prime_kernel<RECV_PULL, PM, true, false>;
+}
+
+// The step kernel instance for the current run parameters: the lean tiled
+// instance when nothing is recorded or counted.
+StepFn run_fn(const snp_engine* e) {
+    if (e->lean_fn && e->hctrl.record == 0 && !e->hctrl.stats_on) return e->lean_fn;
+    return e->step_fn;
+}
+
 int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullptr) {
     const long long q = d->q, m = d->m;
     if (q < 0 || m < 0) return fail(SNP_ERR_BAD_ARG, "q and m must be >= 0");
@@ -448,6 +500,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         e->variant = SNP_VARIANT_PUSH;
         e->kind = RECV_ARRAY;
     }
+    e->p_max = pmax;
     if (pcommon) {
         e->p_mode = P_BIT;
         e->p_common = pfirst > 0 ? pfirst : 1;
@@ -640,15 +693,11 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
 
     // kernel instances
     if (e->tiled) {
-        auto pick = [&](auto wide_k, auto narrow_k, PrimeFn prime) {
-            e->step_fn = e->wide_rules ? wide_k : narrow_k;
-            e->prime_fn = prime;
-        };
         switch (e->p_mode) {
-            case P_BIT: pick(tiled_step_kernel<P_BIT, true>, tiled_step_kernel<P_BIT, false>, prime_kernel<RECV_PULL, P_BIT, true, false>); break;
-            case P_U8: pick(tiled_step_kernel<P_U8, true>, tiled_step_kernel<P_U8, false>, prime_kernel<RECV_PULL, P_U8, true, false>); break;
-            case P_U16: pick(tiled_step_kernel<P_U16, true>, tiled_step_kernel<P_U16, false>, prime_kernel<RECV_PULL, P_U16, true, false>); break;
-            default: pick(tiled_step_kernel<P_U32, true>, tiled_step_kernel<P_U32, false>, prime_kernel<RECV_PULL, P_U32, true, false>); break;
+            case P_BIT: pick_tiled<P_BIT>(e); break;
+            case P_U8: pick_tiled<P_U8>(e); break;
+            case P_U16: pick_tiled<P_U16>(e); break;
+            default: pick_tiled<P_U32>(e); break;
         }
     } else if (e->format == SNP_FMT_COMPRESSED && e->kind == RECV_PULL) {
         switch (e->p_mode) {
@@ -669,8 +718,10 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     CU(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, e->device));
     if (e->tiled) {
         e->step_block = kTileThreads + 32;  // consumer warps + one TMA producer warp
-        e->step_smem = (size_t)kRingStages * kStageBytes + (size_t)(s.tile + 1) * sizeof(uint32_t);
+        e->step_smem = (size_t)s.ring * kStageBytes +
+                       (size_t)(e->acc16 ? acc_words<true>(s.tile) : acc_words<false>(s.tile)) * sizeof(uint32_t);
         CU(cudaFuncSetAttribute(e->step_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
+        CU(cudaFuncSetAttribute(e->lean_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, e->step_block, e->step_smem));
         const long long resident = (long long)std::max(1, per_sm) * std::max(1, n_sm);
         e->step_grid = (int)std::min<long long>(s.n_tiles, resident);
@@ -690,7 +741,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
 // Launch one step's kernels on the engine stream; returns launch count.
 int launch_step(snp_engine* e, long long* row_visits = nullptr) {
     int n = 1;
-    e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
+    run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
     if (e->kind == RECV_ARRAY) {
         if (e->format == SNP_FMT_SPARSE) {
             dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
@@ -767,7 +818,7 @@ int ensure_trace(snp_engine* e, long long rows) {
 }
 
 int ensure_graph(snp_engine* e, long long iters) {
-    if (e->graph && e->graph_iters == iters) return SNP_OK;
+    if (e->graph && e->graph_iters == iters && e->graph_fn == run_fn(e)) return SNP_OK;
     if (e->graph) {
         cudaGraphExecDestroy(e->graph);
         e->graph = nullptr;
@@ -780,6 +831,7 @@ int ensure_graph(snp_engine* e, long long iters) {
     cudaGraphDestroy(g);
     CU(err);
     e->graph_iters = iters;
+    e->graph_fn = run_fn(e);
     return SNP_OK;
 }
 
@@ -900,6 +952,9 @@ int snp_engine_get_info(const snp_engine* e, snp_engine_info* info) {
     info->p_common = e->p_common;
     info->tile = e->sys.tile;
     info->n_tiles = e->sys.n_tiles;
+    info->ring_stages = e->tiled ? e->sys.ring : 0;
+    info->counter_bits = e->tiled ? (e->acc16 ? 16 : 32) : 0;
+    info->stage_bytes = e->tiled ? (int64_t)kStageBytes : 0;
     return SNP_OK;
 }
 
@@ -1052,7 +1107,7 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
         CU(cudaEventRecord(e->ev0, e->stream));
         for (long long i = 0; i < steps; ++i) {
             CU(cudaEventRecord(ev[2 * i], e->stream));
-            e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
+            run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
             CU(cudaEventRecord(ev[2 * i + 1], e->stream));
             launches += 1;
             if (e->kind == RECV_ARRAY) {

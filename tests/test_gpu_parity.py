@@ -147,6 +147,26 @@ def test_full_size_synth_steps_bit_exact(delays, policy):
     assert res.steps == steps and res.halt_reason is snp.HaltReason.STEP_LIMIT
 
 
+@pytest.mark.parametrize("delays,policy", [(False, 0), (True, 0), (False, 1), (True, 1)])
+def test_lean_kernel_many_steps_bit_exact(delays, policy):
+    """Unrecorded runs take the lean tiled instance (no trace / counters, fast
+    phase-2 selection); 60 steps of it must equal the C oracle and the final
+    row of a recorded (non-lean) run."""
+    q, steps = 300_000, 60
+    a = snp.synth_v1(q, with_delays=delays)
+    sel = snp.FirstApplicable() if policy == 0 else snp.SeededRandom(2**63 + 5)
+    seed = 0 if policy == 0 else 2**63 + 5
+    prep = snp.prepare(a, snp.Format.COMPRESSED)
+    res = snp.run_final(prep, snp.SimOptions(max_steps=steps, selection=sel))
+    _, want_c, want_d = coracle.run(OracleSystem.from_arrays(a), steps, policy, seed)
+    np.testing.assert_array_equal(res.config, want_c)
+    np.testing.assert_array_equal(res.delays, want_d)
+    tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=steps, selection=sel,
+                                                    record=snp.RecordLevel.CONFIGS_AND_DELAYS))
+    np.testing.assert_array_equal(tr.configs[-1], want_c)
+    np.testing.assert_array_equal(tr.delays[-1], want_d)
+
+
 def test_full_size_formats_agree():
     """ELL and push-Optimized reach the same state as pull-Optimized at 10^7."""
     a = snp.synth_v1(10_000_000, with_delays=True)

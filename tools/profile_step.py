@@ -25,4 +25,4 @@ prep.engine.begin()
 tot, kms, _ = prep.engine.time_steps(a.steps, sel, per_kernel=True)
 info = prep.engine.info
 print(f"{a.workload}/{a.format}/{a.variant}/{a.policy}: {tot / a.steps:.3f} ms/step, step kernel {kms:.3f} ms "
-      f"tile={info['tile']} n_tiles={info['n_tiles']} words={info['in_edges']} dev_MB={info['device_bytes'] >> 20}")
+      f"tile={info['tile']} n_tiles={info['n_tiles']} ring={info.get('ring_stages')}x{info.get('stage_bytes')} acc{info.get('counter_bits')} words={info['in_edges']} dev_MB={info['device_bytes'] >> 20}")
