@@ -15,13 +15,28 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
 
 
+IO_SOURCES = [PKG / "csrc" / "snp_modelio.cpp"]
+IO_DEPS = IO_SOURCES + [PKG.parent / "include" / "snpio.h"]
+IO_OUT = PKG / "libsnpio.so"
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wextra"]
+
+
+def _stale(out: Path, deps: list[Path]) -> bool:
+    return not out.exists() or any(out.stat().st_mtime < d.stat().st_mtime for d in deps)
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and OUT.exists() and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in DEPS):
-        return OUT
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", str(OUT), *map(str, SOURCES)]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+    """Build libsnpb200.so (nvcc, sm_100a) and libsnpio.so (g++, host-only
+    model-file I/O)."""
+    jobs = []
+    if force or _stale(OUT, DEPS):
+        jobs.append(["nvcc", *NVCC_FLAGS, "-o", str(OUT), *map(str, SOURCES)])
+    if force or _stale(IO_OUT, IO_DEPS):
+        jobs.append(["g++", *CXX_FLAGS, "-o", str(IO_OUT), *map(str, IO_SOURCES)])
+    for cmd in jobs:
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
     return OUT
 
 

@@ -249,17 +249,19 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         unsigned long long e2 = start[t];
         const unsigned long long end = start[t + 1];
         while (e2 < end) {
-            const uint32_t b = bsrc[e2];
+            // bases are multiples of 32 so that an offset's low 5 bits index
+            // the bit inside a P word (tiled_step_kernel phase 1)
+            const uint32_t b = bsrc[e2] & ~31u;
             base.push_back(b);
             int n = 0;
             while (e2 < end && n < kSegEdges && bsrc[e2] - b < kSrcSpan) {
-                words.push_back(((bsrc[e2] - b) << kDstBits) | bslot[e2]);
+                words.push_back(((uint32_t)bslot[e2] << kSrcBits) | (bsrc[e2] - b));
                 ++e2;
                 ++n;
             }
             last.push_back(bsrc[e2 - 1]);
             // padding: source offset 0 (inside the window), dummy counter slot T
-            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T);
+            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T << kSrcBits);
         }
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");

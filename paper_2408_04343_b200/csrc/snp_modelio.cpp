@@ -1,0 +1,455 @@
+// snp_modelio.cpp -- native model-file parser and writer (include/snpio.h).
+//
+// Same grammar, checks, check order and messages as the reference's
+// parse_model / serialize_model (pkg/src/snpsim/modelfile.py:40-143) and the
+// builder invariants it triggers (model.py:50-112 SpikeRegex/Rule,
+// model.py:155-180 add_neuron/add_rule/add_synapse), but single pass over a
+// byte buffer into flat arrays: rules are regrouped by owner with a stable
+// counting pass (validate(), model.py:251) and synapses become a sorted,
+// de-duplicated CSR (model.py:255-257).
+//
+// Deviations (documented in DESIGN.md): integers must fit int64 (the
+// reference's Python ints are unbounded; larger values would fail the
+// engine's int32/int64 range checks anyway), neuron counts must be < 2^32,
+// and only ASCII line breaks / whitespace are recognised.
+#include <algorithm>
+#include <cerrno>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/snpio.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+// Python repr() of a str made of the given bytes (ASCII escapes; other
+// bytes pass through as UTF-8).
+std::string py_repr(const char* p, size_t n) {
+    bool has_sq = memchr(p, '\'', n) != nullptr, has_dq = memchr(p, '"', n) != nullptr;
+    const char q = (has_sq && !has_dq) ? '"' : '\'';
+    std::string s(1, q);
+    for (size_t i = 0; i < n; ++i) {
+        const unsigned char c = (unsigned char)p[i];
+        if (c == '\\') s += "\\\\";
+        else if (c == (unsigned char)q) { s += '\\'; s += (char)c; }
+        else if (c == '\t') s += "\\t";
+        else if (c == '\n') s += "\\n";
+        else if (c == '\r') s += "\\r";
+        else if (c < 0x20 || c == 0x7f) {
+            char b[8];
+            snprintf(b, sizeof(b), "\\x%02x", c);
+            s += b;
+        } else s += (char)c;
+    }
+    s += q;
+    return s;
+}
+
+inline bool is_break(unsigned char c) { return c == '\n' || c == '\r' || c == '\v' || c == '\f' || (c >= 0x1c && c <= 0x1e); }
+inline bool is_space(unsigned char c) { return c == ' ' || c == '\t' || is_break(c) || c == 0x1f; }
+
+struct Tok {
+    const char* p;
+    size_t n;
+    bool is(const char* s) const { return strlen(s) == n && memcmp(p, s, n) == 0; }
+    std::string repr() const { return py_repr(p, n); }
+};
+
+// int(token) as Python parses it: optional sign, digits with single
+// underscores between them.  0 ok, 1 not an integer, 2 outside int64.
+int parse_int(const Tok& t, long long* out) {
+    size_t i = 0;
+    bool neg = false;
+    if (i < t.n && (t.p[i] == '+' || t.p[i] == '-')) neg = t.p[i++] == '-';
+    if (i >= t.n) return 1;
+    unsigned long long v = 0;
+    bool over = false, prev_digit = false;
+    for (; i < t.n; ++i) {
+        const char c = t.p[i];
+        if (c == '_') {
+            if (!prev_digit || i + 1 >= t.n) return 1;
+            prev_digit = false;
+            continue;
+        }
+        if (c < '0' || c > '9') return 1;
+        prev_digit = true;
+        if (v > (~0ull - 9) / 10) over = true;
+        v = v * 10 + (unsigned long long)(c - '0');
+        if (v > (1ull << 63)) over = true;
+    }
+    if (!prev_digit) return 1;
+    if (over || (!neg && v > (unsigned long long)INT64_MAX)) return 2;
+    *out = neg ? (long long)(0ull - v) : (long long)v;
+    return 0;
+}
+
+}  // namespace
+
+struct snpio_model {
+    std::vector<long long> initial;
+    // rules in file order (regrouped by owner in export)
+    std::vector<uint32_t> owner;
+    std::vector<long long> thr, cons, prod, dly;
+    std::vector<uint8_t> exact;
+    std::vector<unsigned long long> syn;  // src << 32 | dst, file order (duplicates allowed)
+    long long output = -1;
+    // CSR built at the end of parsing
+    std::vector<long long> adj_off, adj_dst;
+};
+
+namespace {
+
+struct Parser {
+    snpio_model* m = nullptr;
+    long long lineno = 0;
+    std::vector<Tok> args;
+
+    int ferr(const char* fmt, ...) {
+        char buf[900];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        return fail(SNPIO_ERR_FORMAT, "line %lld: %s", lineno, buf);
+    }
+    // modelfile.py:151-160
+    int get_int(size_t pos, const char* what, long long* v) {
+        if (pos >= args.size()) return ferr("missing %s", what);
+        const int rc = parse_int(args[pos], v);
+        if (rc == 1) return ferr("%s must be an integer, got %s", what, args[pos].repr().c_str());
+        if (rc == 2) return ferr("%s out of range for the native parser, got %s", what, args[pos].repr().c_str());
+        return SNPIO_OK;
+    }
+    // modelfile.py:163-167
+    int get_index(size_t pos, long long count, long long* v) {
+        long long x;
+        if (int rc = get_int(pos, "neuron index", &x)) return rc;
+        if (x < 1 || x > count) return ferr("neuron index %lld out of range 1..%lld", x, count);
+        *v = x - 1;
+        return SNPIO_OK;
+    }
+
+    int run(const char* text, size_t len) {
+        bool header = false, spikes = false;
+        long long count = -1;
+        size_t i = 0;
+        while (i < len) {
+            // one line (str.splitlines: \r\n counts once)
+            size_t e = i;
+            while (e < len && !is_break((unsigned char)text[e])) ++e;
+            const char* raw = text + i;
+            const size_t raw_n = e - i;
+            size_t next = e;
+            if (next < len) next += (text[next] == '\r' && next + 1 < len && text[next + 1] == '\n') ? 2 : 1;
+            i = next;
+            ++lineno;
+            const char* hash = (const char*)memchr(raw, '#', raw_n);
+            const size_t n = hash ? (size_t)(hash - raw) : raw_n;
+            args.clear();
+            for (size_t k = 0; k < n;) {
+                while (k < n && is_space((unsigned char)raw[k])) ++k;
+                size_t b = k;
+                while (k < n && !is_space((unsigned char)raw[k])) ++k;
+                if (k > b) args.push_back(Tok{raw + b, k - b});
+            }
+            if (args.empty()) continue;
+            const Tok key = args.front();
+            args.erase(args.begin());
+            if (!header) {
+                if (!key.is("snp"))
+                    return ferr("expected 'snp <version>' header, got %s", py_repr(raw, raw_n).c_str());
+                long long ver;
+                if (int rc = get_int(0, "format version", &ver)) return rc;
+                if (ver != 1) return ferr("unsupported format version %lld", ver);
+                header = true;
+            } else if (key.is("neurons")) {
+                if (count >= 0) return ferr("duplicate 'neurons' line");
+                if (int rc = get_int(0, "neuron count", &count)) return rc;
+                if (count < 0) return ferr("neuron count must be >= 0");
+                if (count >= (1ll << 32) - 1) return ferr("neuron count %lld too large for the native parser", count);
+            } else if (key.is("spikes")) {
+                if (count < 0) return ferr("'spikes' before 'neurons'");
+                if (spikes) return ferr("duplicate 'spikes' line");
+                if ((long long)args.size() != count)
+                    return ferr("expected %lld spike counts, got %zu", count, args.size());
+                m->initial.reserve((size_t)count);
+                for (long long p = 0; p < count; ++p) {
+                    long long v;
+                    if (int rc = get_int((size_t)p, "spike count", &v)) return rc;
+                    if (v < 0) return fail(SNPIO_ERR_MODEL, "initial spike count must be >= 0, got %lld", v);
+                    m->initial.push_back(v);
+                }
+                spikes = true;
+            } else if (key.is("rule") || key.is("synapse") || key.is("output")) {
+                if (!spikes) return ferr("directive before 'spikes' line");
+                if (key.is("rule")) {
+                    if (args.size() != 6) return ferr("'rule' needs 6 fields, got %zu", args.size());
+                    int exact;
+                    if (args[1].is("ge")) exact = 0;
+                    else if (args[1].is("eq")) exact = 1;
+                    else return ferr("condition kind must be 'ge' or 'eq', got %s", args[1].repr().c_str());
+                    long long own = 0, t = 0, c = 0, p = 0, d = 0;
+                    if (int rc = get_index(0, count, &own)) return rc;
+                    if (int rc = get_int(2, "threshold", &t)) return rc;
+                    // SpikeRegex (model.py:50-55)
+                    if (t < 0) return fail(SNPIO_ERR_INVALID_RULE, "condition threshold must be >= 0, got %lld", t);
+                    if (exact && t < 1) return fail(SNPIO_ERR_INVALID_RULE, "an exact-count condition needs threshold >= 1");
+                    if (int rc = get_int(3, "consumed", &c)) return rc;
+                    if (int rc = get_int(4, "produced", &p)) return rc;
+                    if (int rc = get_int(5, "delay", &d)) return rc;
+                    // Rule (model.py:87-106)
+                    if (c < 1) return fail(SNPIO_ERR_INVALID_RULE, "a rule must consume at least one spike, got %lld", c);
+                    if (p < 0) return fail(SNPIO_ERR_INVALID_RULE, "produced spike count must be >= 0, got %lld", p);
+                    if (d < 0) return fail(SNPIO_ERR_INVALID_RULE, "delay must be >= 0, got %lld", d);
+                    if (p == 0) {
+                        if (d != 0) return fail(SNPIO_ERR_INVALID_RULE, "a forgetting rule cannot carry a delay");
+                        if (!exact || t != c)
+                            return fail(SNPIO_ERR_INVALID_RULE, "a forgetting rule must be guarded by exactly its consumed count");
+                    } else if (p > c) {
+                        return fail(SNPIO_ERR_INVALID_RULE,
+                                    "a firing rule cannot produce more than it consumes (consumed=%lld, produced=%lld)", c, p);
+                    }
+                    m->owner.push_back((uint32_t)own);
+                    m->thr.push_back(t);
+                    m->exact.push_back((uint8_t)exact);
+                    m->cons.push_back(c);
+                    m->prod.push_back(p);
+                    m->dly.push_back(d);
+                } else if (key.is("synapse")) {
+                    if (args.size() != 2) return ferr("'synapse' needs 2 fields");
+                    long long a = 0, b = 0;
+                    if (int rc = get_index(0, count, &a)) return rc;
+                    if (int rc = get_index(1, count, &b)) return rc;
+                    if (a == b) return fail(SNPIO_ERR_REFLEXIVE, "synapse (%lld, %lld) is reflexive", a, a);
+                    m->syn.push_back(((unsigned long long)a << 32) | (unsigned long long)b);
+                } else {
+                    if (int rc = get_index(0, count, &m->output)) return rc;
+                }
+            } else {
+                return ferr("unknown directive %s", key.repr().c_str());
+            }
+        }
+        if (!header) return fail(SNPIO_ERR_FORMAT, "empty model file");
+        if (count < 0 || !spikes) return fail(SNPIO_ERR_FORMAT, "model file is missing 'neurons' or 'spikes'");
+        return finish((size_t)count);
+    }
+
+    // validate(): synapses -> ascending, de-duplicated CSR
+    int finish(size_t q) {
+        std::vector<long long>& off = m->adj_off;
+        off.assign(q + 1, 0);
+        for (unsigned long long x : m->syn) off[(x >> 32) + 1]++;
+        for (size_t v = 0; v < q; ++v) off[v + 1] += off[v];
+        std::vector<uint32_t> dst(m->syn.size());
+        {
+            std::vector<long long> cur(off.begin(), off.end() - 1);
+            for (unsigned long long x : m->syn) dst[(size_t)cur[x >> 32]++] = (uint32_t)x;
+        }
+        std::vector<unsigned long long>().swap(m->syn);
+        m->adj_dst.reserve(dst.size());
+        long long w = 0;
+        for (size_t v = 0; v < q; ++v) {
+            auto b = dst.begin() + off[v], e = dst.begin() + off[v + 1];
+            std::sort(b, e);
+            e = std::unique(b, e);
+            off[v] = w;
+            for (auto it = b; it != e; ++it) m->adj_dst.push_back(*it);
+            w += (long long)(e - b);
+        }
+        off[q] = w;
+        return SNPIO_OK;
+    }
+};
+
+// ---- writer
+
+struct Out {
+    FILE* f;
+    std::vector<char> buf;
+    size_t n = 0;
+    explicit Out(FILE* f_) : f(f_), buf(1 << 22) {}
+    bool flush() {
+        if (n && fwrite(buf.data(), 1, n, f) != n) return false;
+        n = 0;
+        return true;
+    }
+    bool room(size_t k) { return (buf.size() - n >= k) || flush(); }
+    void put(const char* s) {
+        while (*s) buf[n++] = *s++;
+    }
+    void put(char c) { buf[n++] = c; }
+    void num(long long v) {
+        char t[24];
+        int k = 0;
+        unsigned long long u = v < 0 ? 0ull - (unsigned long long)v : (unsigned long long)v;
+        do {
+            t[k++] = (char)('0' + u % 10);
+            u /= 10;
+        } while (u);
+        if (v < 0) buf[n++] = '-';
+        while (k) buf[n++] = t[--k];
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* snpio_last_error(void) { return g_err.c_str(); }
+
+int snpio_parse(const char* text, int64_t len, snpio_model** out) {
+    if (!out || (!text && len > 0) || len < 0) return fail(SNPIO_ERR_IO, "bad arguments");
+    *out = nullptr;
+    try {
+        auto* m = new snpio_model();
+        Parser p;
+        p.m = m;
+        int rc = p.run(text, (size_t)len);
+        if (rc != SNPIO_OK) {
+            delete m;
+            return rc;
+        }
+        *out = m;
+        return SNPIO_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(SNPIO_ERR_NOMEM, "out of host memory while parsing the model file");
+    }
+}
+
+int snpio_parse_file(const char* path, snpio_model** out) {
+    if (!path || !out) return fail(SNPIO_ERR_IO, "bad arguments");
+    FILE* f = fopen(path, "rb");
+    if (!f) return fail(SNPIO_ERR_IO, "cannot open %s: %s", path, strerror(errno));
+    std::vector<char> data;
+    try {
+        if (fseek(f, 0, SEEK_END) == 0) {
+            const long sz = ftell(f);
+            if (sz > 0) data.resize((size_t)sz);
+            fseek(f, 0, SEEK_SET);
+        }
+        size_t got = data.empty() ? 0 : fread(data.data(), 1, data.size(), f);
+        data.resize(got);
+    } catch (const std::bad_alloc&) {
+        fclose(f);
+        return fail(SNPIO_ERR_NOMEM, "out of host memory reading %s", path);
+    }
+    fclose(f);
+    return snpio_parse(data.data(), (int64_t)data.size(), out);
+}
+
+int snpio_model_sizes(const snpio_model* m, int64_t* q, int64_t* nr, int64_t* s, int64_t* output) {
+    if (!m) return fail(SNPIO_ERR_IO, "null model");
+    if (q) *q = (int64_t)m->initial.size();
+    if (nr) *nr = (int64_t)m->owner.size();
+    if (s) *s = (int64_t)m->adj_dst.size();
+    if (output) *output = m->output;
+    return SNPIO_OK;
+}
+
+int snpio_model_export(const snpio_model* m, int64_t* initial, int64_t* offsets, int64_t* threshold,
+                       uint8_t* is_exact, int64_t* consumed, int64_t* produced, int64_t* delay,
+                       int64_t* adj_offsets, int64_t* adj_targets) {
+    if (!m) return fail(SNPIO_ERR_IO, "null model");
+    const size_t q = m->initial.size(), nr = m->owner.size();
+    if (initial) std::copy(m->initial.begin(), m->initial.end(), initial);
+    // stable regroup of rules by owner (validate(), model.py:251)
+    std::vector<long long> off(q + 1, 0);
+    for (uint32_t o : m->owner) off[o + 1]++;
+    for (size_t v = 0; v < q; ++v) off[v + 1] += off[v];
+    if (offsets) std::copy(off.begin(), off.end(), offsets);
+    std::vector<long long> cur(off.begin(), off.end() - (q ? 1 : 0));
+    for (size_t r = 0; r < nr; ++r) {
+        const size_t at = (size_t)cur[m->owner[r]]++;
+        if (threshold) threshold[at] = m->thr[r];
+        if (is_exact) is_exact[at] = m->exact[r];
+        if (consumed) consumed[at] = m->cons[r];
+        if (produced) produced[at] = m->prod[r];
+        if (delay) delay[at] = m->dly[r];
+    }
+    if (adj_offsets) std::copy(m->adj_off.begin(), m->adj_off.end(), adj_offsets);
+    if (adj_targets) std::copy(m->adj_dst.begin(), m->adj_dst.end(), adj_targets);
+    return SNPIO_OK;
+}
+
+void snpio_model_free(snpio_model* m) { delete m; }
+
+int snpio_write_file(const char* path, int64_t q, int64_t m, int64_t s, const int64_t* initial,
+                     const int64_t* offsets, const int64_t* threshold, const uint8_t* is_exact,
+                     const int64_t* consumed, const int64_t* produced, const int64_t* delay,
+                     const int64_t* adj_offsets, const int64_t* adj_targets, int64_t output) {
+    if (!path || q < 0 || m < 0 || s < 0) return fail(SNPIO_ERR_IO, "bad arguments");
+    if ((q && (!initial || !offsets || !adj_offsets)) || (m && (!threshold || !is_exact || !consumed || !produced || !delay)) ||
+        (s && !adj_targets))
+        return fail(SNPIO_ERR_IO, "missing arrays");
+    FILE* f = fopen(path, "wb");
+    if (!f) return fail(SNPIO_ERR_IO, "cannot open %s: %s", path, strerror(errno));
+    bool ok = true;
+    try {
+        Out o(f);
+        ok = o.room(64);
+        o.put("snp 1\nneurons ");
+        o.num(q);
+        o.put("\nspikes");
+        for (int64_t i = 0; ok && i < q; ++i) {
+            ok = o.room(32);
+            o.put(' ');
+            o.num(initial[i]);
+        }
+        o.put('\n');
+        for (int64_t v = 0; ok && v < q; ++v) {
+            for (int64_t r = offsets[v]; ok && r < offsets[v + 1]; ++r) {
+                ok = o.room(160);
+                o.put("rule ");
+                o.num(v + 1);
+                o.put(is_exact[r] ? " eq " : " ge ");
+                o.num(threshold[r]);
+                o.put(' ');
+                o.num(consumed[r]);
+                o.put(' ');
+                o.num(produced[r]);
+                o.put(' ');
+                o.num(delay[r]);
+                o.put('\n');
+            }
+        }
+        for (int64_t v = 0; ok && v < q; ++v) {
+            for (int64_t x = adj_offsets[v]; ok && x < adj_offsets[v + 1]; ++x) {
+                ok = o.room(64);
+                o.put("synapse ");
+                o.num(v + 1);
+                o.put(' ');
+                o.num(adj_targets[x] + 1);
+                o.put('\n');
+            }
+        }
+        if (ok && output >= 0) {
+            ok = o.room(32);
+            o.put("output ");
+            o.num(output + 1);
+            o.put('\n');
+        }
+        ok = ok && o.flush();
+    } catch (const std::bad_alloc&) {
+        fclose(f);
+        return fail(SNPIO_ERR_NOMEM, "out of host memory writing %s", path);
+    }
+    if (fclose(f) != 0) ok = false;
+    return ok ? SNPIO_OK : fail(SNPIO_ERR_IO, "write to %s failed", path);
+}
+
+}  // extern "C"
