@@ -54,10 +54,7 @@ constexpr int kTileThreads = SNP_TILE_THREADS;  // consumer threads per CTA (mul
 static_assert(kTileThreads % 32 == 0 && kTileThreads + 32 <= 1024, "CTA must fit 1024 threads");
 constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
 constexpr uint32_t kDstBits = 15;         // destination slot within a tile
-constexpr uint32_t kSrcBits = 17;         // source offset within a segment
-constexpr uint32_t kSrcSpan = 1u << kSrcBits;
-constexpr uint32_t kSrcMask = kSrcSpan - 1u;
-static_assert(kDstBits + kSrcBits == 32, "segment words are 32 bits");
+constexpr uint32_t kSrcSpan = 1u << 17;   // source offset range within a segment
 constexpr uint32_t kDummyEdge = 0xffffffffu;  // CSR / legacy padding marker
 constexpr int kMaxTile = (1 << kDstBits) - 32;
 enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
@@ -118,8 +115,8 @@ struct DevSys {
     int ell_rows;             // z + 1
     long long p_common;       // P_BIT: the single produced amount
     // tiled pull (default COMPRESSED kernel)
-    const uint32_t* seg_words;  // [nseg * kSegEdges] dst slot << kSrcBits | (src - seg_base)
-    const uint32_t* seg_base;   // [nseg] first source of each segment, rounded down to 32
+    const uint32_t* seg_words;  // [nseg * kSegEdges] (src - seg_base) << kDstBits | dst slot
+    const uint32_t* seg_base;   // [nseg] first source of each segment
     const StageDesc* stages;    // TMA stage descriptors, tile-major (build_tiles)
     const uint32_t* tstage;     // [n_tiles + 1] stage range of each tile
     const uint32_t* stage_bases;  // segment bases per phase-1 stage (16-byte aligned runs)
@@ -825,7 +822,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 //
 // A CTA owns a tile of `s.tile` consecutive destinations.  Their in-edges are
 // stored sorted by source and cut into 256-edge segments whose sources span
-// < 2^17 (host build: build_tiles), each word = slot << 17 | (src - seg_base).
+// < 2^17 (host build: build_tiles), each word = (src - seg_base) << 15 | slot.
 // Warp-specialised: one producer warp streams everything the tile needs from
 // HBM through a kRingStages-deep TMA ring in shared memory (cp.async.bulk,
 // full/empty mbarriers); the consumer warps never wait on each other except
@@ -1049,37 +1046,31 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     // Padding edges are (0, slot T): a real lookup into the
                     // dummy counter, so the loop has no branches.
                     const uint32_t base = h->bases[i];
+                    const uint32_t rel0 = base - src0;
                     const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf + kPayload + i * kSegEdges * 4u) + lane;
                     uint32_t w[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) w[e] = wp[e * 32];
-                    // word = slot << 17 | source offset; base and src0 are multiples
-                    // of 32, so the offset's low 5 bits are the bit inside a P word
-                    // and every address below is one mask + one shifted add
                     auto add = [&](uint32_t we, uint32_t v) {
-                        if (A16) {
-                            uint32_t* a = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(acc) + ((we & 0xfffc0000u) >> 16));
-                            atomicAdd(a, v << ((we >> 13) & 16u));
-                        } else {
-                            atomicAdd(reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(acc) + ((we & 0xfffe0000u) >> 15)), v);
-                        }
+                        const uint32_t slot = we & ((1u << kDstBits) - 1u);
+                        if (A16) atomicAdd(&acc[slot >> 1], v << ((slot & 1u) << 4));
+                        else atomicAdd(&acc[slot], v);
                     };
                     if (PM == P_BIT && pst) {
-                        const uint8_t* pseg = reinterpret_cast<const uint8_t*>(ps) + ((base - src0) >> 3);
 #pragma unroll
                         for (int e = 0; e < 8; ++e) {
-                            const uint32_t pw = *reinterpret_cast<const uint32_t*>(pseg + ((w[e] & (kSrcMask & ~31u)) >> 3));
-                            add(w[e], __funnelshift_r(pw, 0u, w[e]) & 1u);
+                            const uint32_t rel = rel0 + (w[e] >> kDstBits);
+                            add(w[e], (ps[rel >> 5] >> (rel & 31)) & 1u);  // src0 is a multiple of 128
                         }
                     } else {
                         // P looked up in global memory (L1/L2): non-bit P, or
                         // windows not staged
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) add(w[e], (uint32_t)p_lookup<PM>(Pprev, base + (w[e] & kSrcMask)));
+                        for (int e = 0; e < 8; ++e) add(w[e], (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits)));
                     }
                     if (stats_on) {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) stat[ST_EDGES] += ((w[e] >> kSrcBits) != (uint32_t)T);
+                        for (int e = 0; e < 8; ++e) stat[ST_EDGES] += ((w[e] & ((1u << kDstBits) - 1u)) != (uint32_t)T);
                     }
                 }
                 __syncwarp();

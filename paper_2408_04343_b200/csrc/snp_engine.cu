@@ -196,7 +196,9 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         if (const char* env = getenv("SNPB200_ACC16")) e->acc16 = e->acc16 && atoi(env) != 0;
     }
     // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
-    long long T = ceil_div(std::max<long long>(q, 1), 4ll * n_sm);
+    // (3 tiles per SM with 16-bit counters leaves room for a 3 x 48 KB ring;
+    // 4 per SM with 32-bit counters; measured on K3, profiles/r1_history.md)
+    long long T = ceil_div(std::max<long long>(q, 1), (e->acc16 ? 3ll : 4ll) * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
     if (const char* env = getenv("SNPB200_TILE")) T = atoll(env);
     // shared memory: the TMA ring (2..kMaxRing stages) plus the destination
@@ -249,19 +251,17 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         unsigned long long e2 = start[t];
         const unsigned long long end = start[t + 1];
         while (e2 < end) {
-            // bases are multiples of 32 so that an offset's low 5 bits index
-            // the bit inside a P word (tiled_step_kernel phase 1)
-            const uint32_t b = bsrc[e2] & ~31u;
+            const uint32_t b = bsrc[e2];
             base.push_back(b);
             int n = 0;
             while (e2 < end && n < kSegEdges && bsrc[e2] - b < kSrcSpan) {
-                words.push_back(((uint32_t)bslot[e2] << kSrcBits) | (bsrc[e2] - b));
+                words.push_back(((bsrc[e2] - b) << kDstBits) | bslot[e2]);
                 ++e2;
                 ++n;
             }
             last.push_back(bsrc[e2 - 1]);
             // padding: source offset 0 (inside the window), dummy counter slot T
-            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T << kSrcBits);
+            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T);
         }
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
