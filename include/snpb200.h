@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SNPB200_ABI_VERSION 3
+#define SNPB200_ABI_VERSION 4
 
 enum {
     SNP_OK = 0,
@@ -59,7 +59,7 @@ enum { SNP_REC_CONFIGS = 1, SNP_REC_DELAYS = 2, SNP_REC_SPIKING = 4 };
 
 /* engine.py:57-59 HaltReason */
 enum { SNP_RUNNING = 0, SNP_HALT_STEP_LIMIT = 1, SNP_HALT_NO_APPLICABLE = 2,
-       SNP_HALT_NEGATIVE = 3 };
+       SNP_HALT_NEGATIVE = 3, SNP_HALT_EXCHANGE = 4 };
 
 typedef struct snp_system_desc {
     int32_t format;            /* SNP_FMT_* */
@@ -213,6 +213,26 @@ int snp_configure(snp_engine *eng, const snp_run_opts *opts);
 int snp_launch_step(snp_engine *eng);
 /* Synchronise the engine stream and read the run state. */
 int snp_poll(snp_engine *eng, snp_result *res);
+
+/* Peer exchange (NVLink / NVSwitch P2P; replaces the all-gather).  Every
+ * rank's step kernel stores its P chunk and step header straight into each
+ * peer's exchange slot (tile by tile, overlapping the step's own work) and
+ * then raises a per-rank step flag on every peer; the next step kernel waits
+ * for all flags of the previous step.  No collective call per step: after
+ * connecting, the caller only calls snp_launch_step.  Every rank must finish
+ * snp_begin before any rank launches the run's first step (a host barrier).
+ * A rank that stops stepping makes the others halt with SNP_ERR_CUDA
+ * ("peer exchange timed out") after 20 s instead of hanging.
+ *   snp_exchange_ipc_handle: this rank's exchange block as a CUDA IPC handle
+ *     (SNP_IPC_HANDLE_BYTES bytes) to all-gather across processes;
+ *   snp_exchange_connect: map every rank's block (handles[world]) into this
+ *     process and enable peer exchange;
+ *   snp_exchange_connect_local: the same for `world` engines of one process
+ *     (e.g. several ranks on one device). */
+#define SNP_IPC_HANDLE_BYTES 64
+int snp_exchange_ipc_handle(const snp_engine *eng, void *handle);
+int snp_exchange_connect(snp_engine *eng, const void *handles, int world);
+int snp_exchange_connect_local(snp_engine *const *engines, int world);
 
 /* Timing helper for benchmarks: run `steps` steps (no recording) from the
  * current state with the device loop only and return the per-kernel mean

@@ -21,7 +21,8 @@ SNP_OK, SNP_ERR_NEGATIVE, SNP_ERR_BAD_ARG, SNP_ERR_CUDA, SNP_ERR_CAPACITY = rang
 SNP_FMT_SPARSE, SNP_FMT_ELL, SNP_FMT_COMPRESSED = range(3)
 SNP_VARIANT_AUTO, SNP_VARIANT_PULL, SNP_VARIANT_PUSH, SNP_VARIANT_TILED = range(4)
 SNP_REC_CONFIGS, SNP_REC_DELAYS, SNP_REC_SPIKING = 1, 2, 4
-SNP_RUNNING, SNP_HALT_STEP_LIMIT, SNP_HALT_NO_APPLICABLE, SNP_HALT_NEGATIVE = range(4)
+SNP_RUNNING, SNP_HALT_STEP_LIMIT, SNP_HALT_NO_APPLICABLE, SNP_HALT_NEGATIVE, SNP_HALT_EXCHANGE = range(5)
+SNP_IPC_HANDLE_BYTES = 64
 STAT_NAMES = ("steps", "scanned", "fired", "sending", "edges", "rows", "open")
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -115,6 +116,9 @@ SIGNATURES = [
     ("snp_configure", ctypes.c_int, [_EngineP, ctypes.POINTER(RunOpts)]),
     ("snp_launch_step", ctypes.c_int, [_EngineP]),
     ("snp_poll", ctypes.c_int, [_EngineP, ctypes.POINTER(Result)]),
+    ("snp_exchange_ipc_handle", ctypes.c_int, [_EngineP, ctypes.c_void_p]),
+    ("snp_exchange_connect", ctypes.c_int, [_EngineP, ctypes.c_void_p, ctypes.c_int]),
+    ("snp_exchange_connect_local", ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),
     ("snp_time_steps", ctypes.c_int, [_EngineP, ctypes.POINTER(RunOpts), ctypes.c_int64,
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(Result)]),

@@ -59,7 +59,7 @@ constexpr uint32_t kDummyEdge = 0xffffffffu;  // CSR / legacy padding marker
 constexpr int kMaxTile = (1 << kDstBits) - 32;
 enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
 enum Rec { REC_CONFIGS = 1, REC_DELAYS = 2, REC_SPIKING = 4 };
-enum Halt { RUNNING = 0, HALT_STEP_LIMIT = 1, HALT_NO_APPLICABLE = 2, HALT_NEGATIVE = 3 };
+enum Halt { RUNNING = 0, HALT_STEP_LIMIT = 1, HALT_NO_APPLICABLE = 2, HALT_NEGATIVE = 3, HALT_EXCHANGE = 4 };
 enum Stat { ST_STEPS = 0, ST_SCANNED, ST_FIRED, ST_SENDING, ST_EDGES, ST_ROWS, ST_OPEN, ST_COUNT };
 
 // Run-control block in device memory.  Written by the last CTA of each
@@ -86,6 +86,7 @@ struct Ctrl {
     int push_armed;          // a scatter for step (step-1) is pending
     unsigned int list_count[2];   // dense fired-rule list, by step parity
     unsigned int heavy_count[2];  // push heavy queue, by step parity
+    unsigned long long epoch;     // peer exchange: run number (snp_begin), high half of step flags
 };
 
 struct StageDesc;
@@ -95,6 +96,7 @@ struct DevSys {
     long long m;
     const uint32_t* roff;     // [q+1] rule offsets
     const void* rw;           // [m] rule words (compact uint2 / wide uint4), hot path
+    const uint32_t* rw4;      // [m] tiny rule words (tiled, when every rule fits) or null
     const int4* rrec;         // [m] {consumed, produced, delay, 0}, cold paths
     const uint32_t* outdeg;   // [q] out-degree (traffic counters only)
     const uint32_t* ioff;     // pull: [q+1] in-adjacency offsets (4-aligned)
@@ -124,6 +126,7 @@ struct DevSys {
     const uint32_t* theavy;     // [n_tiles + 1] range of s.heavy inside each tile
     int tile;                   // destinations per tile (multiple of 32)
     int ring;                   // TMA ring stages (<= kMaxRing)
+    int rpn;                    // tiled: rules per neuron when every neuron has the same count (<= 32), else 0
     long long n_tiles;
     // row partition (sharded.py): local neuron j is global neuron gbase + j and
     // publishes its P bit at exchange-space position xbase + j; rank r's chunk
@@ -133,6 +136,11 @@ struct DevSys {
     long long x_stride;         // words per rank chunk (0 = not sharded)
     int world;
     int rank;
+    // peer exchange (NVLink P2P): every rank's exchange block (3 slots of
+    // p_words words, then `world` 64-bit step flags), mapped into this process
+    const unsigned long long* peers;
+    long long p_words;
+    int p2p;
 };
 
 struct DevState {
@@ -252,11 +260,69 @@ __device__ __forceinline__ void flush_stats(Ctrl* ctl, unsigned int (&loc)[ST_CO
     if (threadIdx.x < ST_COUNT && sh[threadIdx.x]) atomicAdd(&ctl->stats[threadIdx.x], sh[threadIdx.x]);
 }
 
+// ---- peer exchange (row partition over NVLink P2P, sharded.py)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Step flag value of run `epoch` after step k: monotonic across runs.
+__device__ __forceinline__ unsigned long long step_tag(unsigned long long epoch, long long k) {
+    return (epoch << 32) | (unsigned long long)(k + 1);
+}
+__device__ __forceinline__ uint32_t* peer_slot(const DevSys& s, int r, long long slot) {
+    return reinterpret_cast<uint32_t*>(s.peers[r]) + slot * s.p_words;
+}
+__device__ __forceinline__ unsigned long long* peer_flags(const DevSys& s, int r) {
+    return reinterpret_cast<unsigned long long*>(reinterpret_cast<uint32_t*>(s.peers[r]) + 3 * s.p_words);
+}
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+// Wait until every rank has published step `kdone` (its P chunk and header
+// are in this rank's slot kdone % 3).  Returns false on timeout.
+__device__ __noinline__ bool wait_peers(const DevSys& s, unsigned long long epoch, long long kdone) {
+    const unsigned long long want = step_tag(epoch, kdone);
+    const unsigned long long* fl = peer_flags(s, s.rank);
+    const unsigned long long t0 = globaltimer_ns();
+    for (int r = 0; r < s.world; ++r) {
+        while (ld_acquire_sys(fl + r) < want) {
+            if (globaltimer_ns() - t0 > kPeerTimeoutNs) return false;
+            __nanosleep(100);
+        }
+    }
+    return true;
+}
+
+// Last CTA of a peer-exchange step: this rank's header words (already in its
+// own slot) go to every peer, then the step flag (release) to every rank.
+__device__ __noinline__ void publish_peers(const DevSys& s, long long k, unsigned long long epoch, const uint32_t* hdr) {
+    const long long slot = k % 3;
+    const long long hw = (long long)s.rank * s.x_stride + s.x_stride - 4;
+    for (int r = 0; r < s.world; ++r) {
+        if (r == s.rank) continue;
+        volatile uint32_t* d = peer_slot(s, r, slot) + hw;
+        d[0] = hdr[0];
+        d[1] = hdr[1];
+        d[2] = hdr[2];
+        d[3] = hdr[3];
+    }
+    __threadfence_system();
+    for (int r = 0; r < s.world; ++r) st_release_sys(peer_flags(s, r) + s.rank, step_tag(epoch, k));
+}
+
 // Last-CTA-done: halting decision for step k (engine.py:443-450) and reset
 // of the per-step flags.  Called by thread 0 of every CTA.
 __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bool bf, bool bc,
                                             bool bn, long long neg_idx, long long neg_val,
-                                            uint32_t* xhdr = nullptr) {
+                                            uint32_t* xhdr = nullptr, const DevSys* p2p = nullptr) {
     if (bf) atomicOr(&ctl->fired_any, 1);
     if (bc) atomicOr(&ctl->closed_any, 1);
     if (bn) {
@@ -264,7 +330,8 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
         long long prev = atomicMin(&ctl->neg_index, neg_idx);
         if (neg_idx < prev) ctl->neg_value = neg_val;  // best effort (diagnostics only)
     }
-    __threadfence();
+    if (p2p) __threadfence_system();  // this CTA's peer stores before the flag
+    else __threadfence();
     unsigned int done = atomicAdd(&ctl->blocks_done, 1u);
     if (done != gridDim.x - 1) return;
     __threadfence();
@@ -285,6 +352,7 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
         h[1] = (uint32_t)closed;
         h[2] = (uint32_t)neg;
         h[3] = 0u;
+        if (p2p) publish_peers(*p2p, k, v->epoch, xhdr);
         if (!sel) {
             v->halted = 1;
             v->reason = HALT_STEP_LIMIT;
@@ -319,6 +387,14 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
 // has c < 2^16, p < 2^8, d < 2^8 (one 8-byte word carries everything the
 // step needs, so selection and consumption read one sector per neuron);
 // otherwise wide: uint4 {guard, c, p, d}.
+// Tiny: one 32-bit word per rule for the tiled kernel's staged selection:
+// threshold[9:0] | exact[10] | consumed[20:11] | produced[24:21] | delay[31:25]
+// (host-checked ranges); the compact / wide words stay the general store.
+enum RuleWords { RW_COMPACT = 0, RW_WIDE = 1, RW_TINY = 2 };
+__host__ __device__ constexpr uint32_t tiny_word(uint32_t guard, uint32_t c, uint32_t p, uint32_t d) {
+    return (guard & 0x3ffu) | ((guard & kExactBit) ? 0x400u : 0u) | (c << 11) | (p << 21) | (d << 25);
+}
+
 template <bool WIDE>
 __device__ __forceinline__ uint4 load_rule(const void* __restrict__ rw, uint32_t r) {
     if constexpr (WIDE) {
@@ -472,24 +548,41 @@ __device__ __forceinline__ long long light_commit(const DevSys& s, const DevStat
 // words already in shared memory: the same decisions as light_commit, computed
 // branch-free on a 32-bit saturated count (thresholds are < 2^31).  A negative
 // count selects nothing, as in light_commit (no guard matches C < 0).
-template <int PM>
-__device__ __forceinline__ long long lean_commit4(const DevSys& s, const DevState& st, const StepCtx& cx, long long j,
-                                                  uint32_t nr, const uint2* rp, long long C, int D, bool can_sel,
-                                                  bool& t_fired, bool& t_closed, bool& t_neg, long long& neg_idx,
-                                                  long long& neg_val) {
-    if (C < 0) {
+template <int PM, bool TINY>
+__device__ __forceinline__ long long lean_commit4(const DevSys& s, const DevState& st, Ctrl* ctl, const StepCtx& cx,
+                                                  long long j, uint32_t nr, const void* rpv, long long C, int D,
+                                                  bool can_sel, bool& t_fired, bool& t_closed, bool& t_neg) {
+    if (__builtin_expect(C < 0, 0)) {
+        // NegativeSpikes (engine.py:48-54): rare, reported straight to Ctrl
         t_neg = true;
-        neg_idx = j + s.gbase;
-        neg_val = C;
+        const long long jg = j + s.gbase;
+        if (jg < atomicMin(&ctl->neg_index, jg)) ctl->neg_value = C;
     }
     t_closed |= D != 0;
-    const uint2 w0 = rp[0], w1 = rp[1], w2 = rp[2], w3 = rp[3];
+    // Guard of a rule with threshold t: count in [t, t] (exactly) or [t, inf)
+    // (at least).  With the count saturated to cc <= 2^31 and t < 2^31 that is
+    // one unsigned compare: (cc - t) <= lim, lim = 0 (exactly) or 2^31.
     const uint32_t cc = (C >> 31) != 0 ? 0x80000000u : (uint32_t)C;
-    auto ok = [cc](uint32_t g) -> uint32_t {
-        const uint32_t t = g & ~kExactBit;
-        return (g & kExactBit) ? (cc == t) : (cc >= t);
-    };
-    uint32_t mask = ok(w0.x) | (ok(w1.x) << 1) | (ok(w2.x) << 2) | (ok(w3.x) << 3);
+    uint32_t w[4], y[4];
+    uint32_t mask = 0;
+    if (TINY) {
+        const uint32_t* rp = reinterpret_cast<const uint32_t*>(rpv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w[k] = rp[k];
+            const uint32_t lim = ~(w[k] << 21) & 0x80000000u;  // exact bit 10 -> 31
+            mask |= (cc - (w[k] & 0x3ffu)) <= lim ? (1u << k) : 0u;
+        }
+    } else {
+        const uint2* rp = reinterpret_cast<const uint2*>(rpv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint2 v = rp[k];
+            w[k] = v.x;
+            y[k] = v.y;
+            mask |= (cc - (v.x & ~kExactBit)) <= (~v.x & kExactBit) ? (1u << k) : 0u;
+        }
+    }
     mask &= (can_sel && C >= 0) ? (1u << nr) - 1u : 0u;
     int idx;
     if (cx.policy == 0) {
@@ -497,12 +590,19 @@ __device__ __forceinline__ long long lean_commit4(const DevSys& s, const DevStat
     } else {
         idx = mask ? nth_set_bit(mask, (uint32_t)(mix64(cx.seed, cx.k, j + s.gbase) % (uint32_t)__popc(mask))) : 0;
     }
-    const uint32_t y = idx <= 0 ? w0.y : (idx == 1 ? w1.y : (idx == 2 ? w2.y : w3.y));
+    uint32_t c, p, d;
+    if (TINY) {
+        const uint32_t ws = idx <= 0 ? w[0] : (idx == 1 ? w[1] : (idx == 2 ? w[2] : w[3]));
+        c = (ws >> 11) & 0x3ffu, p = (ws >> 21) & 0xfu, d = ws >> 25;
+    } else {
+        const uint32_t ys = idx <= 0 ? y[0] : (idx == 1 ? y[1] : (idx == 2 ? y[2] : y[3]));
+        c = ys & 0xffffu, p = (ys >> 16) & 0xffu, d = ys >> 24;
+    }
     const bool fired = mask != 0;
     t_fired |= fired;
-    st.cfg[j] = fired ? C - (long long)(y & 0xffffu) : C;
-    st.ds[j] = fired ? -(int)((y >> 24) + 1u) : D;
-    const uint32_t p = fired ? (y >> 16) & 0xffu : 0u;
+    st.cfg[j] = fired ? C - (long long)c : C;
+    st.ds[j] = fired ? -(int)(d + 1u) : D;
+    p = fired ? p : 0u;
     if (PM != P_BIT && cx.sel) {
         if (PM == P_U8) reinterpret_cast<uint8_t*>(cx.Pcur)[j + s.xbase] = (uint8_t)p;
         else if (PM == P_U16) reinterpret_cast<uint16_t*>(cx.Pcur)[j + s.xbase] = (uint16_t)p;
@@ -793,10 +893,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 // global -> shared bulk copy (TMA engine), completion counted on `bar`
@@ -883,8 +983,10 @@ struct StageDesc {
 // (halves the counter footprint, so the ring gets a deeper pipeline).
 // LEAN: no trace recording and no traffic counters (compiled out; the host
 // launches this instance only for runs with record == 0 and stats off).
-template <int PM, bool WIDE, bool A16, bool LEAN>
+template <int PM, int RW, bool A16, bool LEAN>
 __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys s, DevState st) {
+    constexpr bool WIDE = RW == RW_WIDE;
+    constexpr bool TINY = RW == RW_TINY;
     extern __shared__ __align__(128) uint8_t smem[];
     const int nst = s.ring;                                                   // ring stages
     uint8_t* ring = smem;                                                     // nst x kStageBytes
@@ -899,6 +1001,19 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     if (halted || k >= vc->stop_at) {
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->push_armed = 0;
         return;
+    }
+    if (s.p2p && k > 0) {
+        // peer exchange: every rank's step k-1 must be in this rank's slot
+        __shared__ int x_ok;
+        if (threadIdx.x == 0) x_ok = wait_peers(s, vc->epoch, k - 1) ? 1 : 0;
+        __syncthreads();
+        if (!x_ok) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                ctl->halted = 1;
+                ctl->reason = HALT_EXCHANGE;
+            }
+            return;
+        }
     }
     if (s.x_stride && k > 0) {
         // row partition: halting decision for step k-1 from every rank's flags
@@ -954,9 +1069,13 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
 
     if (warp == kWarpsC) {
         // ================= producer warp: descriptors 32 at a time, lane 0 issues the TMA copies
+        // P_{k-1} arrived through generic-proxy stores (this GPU's or peers');
+        // order them before the bulk (async-proxy) reads of the P windows
+        if (s.p2p) asm volatile("fence.proxy.async.global;" ::: "memory");
         int pb = 0;           // next ring stage to fill
         uint32_t pround = 0;  // completed passes over the ring
-        const uint32_t rw_size = WIDE ? 16u : 8u;
+        const uint32_t rw_size = TINY ? 4u : (WIDE ? 16u : 8u);
+        const uint8_t* rw_src = TINY ? reinterpret_cast<const uint8_t*>(s.rw4) : reinterpret_cast<const uint8_t*>(s.rw);
         for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
             const long long d0 = tile * T;
             const uint32_t s0 = __ldg(s.tstage + tile), s1 = __ldg(s.tstage + tile + 1);
@@ -1000,16 +1119,17 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                         } else {
                             // f3 = r_al, f4 = staged rule bytes
                             const long long j0 = d0 + first;
-                            const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u), b_roff = round16((n + 1u) * 4u);
+                            const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u),
+                                           b_roff = s.rpn ? 0u : round16((n + 1u) * 4u);
                             h->r_al = f3;
                             h->rstaged = f4 ? 1u : 0u;
                             mbar_expect_tx(&full_bar[b], b_cfg + b_ds + b_roff + f4);
                             bulk_g2s(buf + kPayload, st.cfg + j0, b_cfg, &full_bar[b]);
                             bulk_g2s(buf + kPayload + b_cfg, st.ds + j0, b_ds, &full_bar[b]);
-                            bulk_g2s(buf + kPayload + b_cfg + b_ds, s.roff + j0, b_roff, &full_bar[b]);
+                            if (b_roff) bulk_g2s(buf + kPayload + b_cfg + b_ds, s.roff + j0, b_roff, &full_bar[b]);
                             if (f4)
                                 bulk_g2s(buf + kPayload + b_cfg + b_ds + b_roff,
-                                         reinterpret_cast<const uint8_t*>(s.rw) + (size_t)f3 * rw_size, f4, &full_bar[b]);
+                                         rw_src + (size_t)f3 * rw_size, f4, &full_bar[b]);
                         }
                     }
                 }
@@ -1090,8 +1210,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 }
                 const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
                 const uint32_t n = h->n, last = h->last, first = h->first, r_al = h->r_al;
-                const bool rstaged = h->rstaged != 0;
-                const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u), b_roff = round16((n + 1u) * 4u);
+                const bool rstaged = h->rstaged != 0;  // staged words are tiny words when TINY
+                const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u),
+                               b_roff = s.rpn ? 0u : round16((n + 1u) * 4u);
                 const long long* cfg_s = reinterpret_cast<const long long*>(buf + kPayload);
                 const int* ds_s = reinterpret_cast<const int*>(buf + kPayload + b_cfg);
                 const uint32_t* roff_s = reinterpret_cast<const uint32_t*>(buf + kPayload + b_cfg + b_ds);
@@ -1104,8 +1225,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 long long Cprev = 0;
                 int dsv = 0;
                 if (active) {
-                    r0 = roff_s[li];
-                    r1 = roff_s[li + 1];
+                    // regular systems (s.rpn rules per neuron) have implicit offsets
+                    r0 = s.rpn ? (uint32_t)(s.rpn * j) : roff_s[li];
+                    r1 = s.rpn ? r0 + (uint32_t)s.rpn : roff_s[li + 1];
                     Cprev = cfg_s[li];
                     dsv = ds_s[li];
                 }
@@ -1122,8 +1244,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                             C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
                         }
                         const int D = ds_next(dsv);
-                        pval = lean_commit4<PM>(s, st, cx, j, nr, reinterpret_cast<const uint2*>(rules_s) + (r0 - r_al),
-                                                C, D, sel && D == 0, t_fired, t_closed, t_neg, neg_idx, neg_val);
+                        const uint8_t* rp = reinterpret_cast<const uint8_t*>(rules_s) + (r0 - r_al) * (TINY ? 4u : 8u);
+                        pval = lean_commit4<PM, TINY>(s, st, ctl, cx, j, nr, rp, C, D, sel && D == 0, t_fired, t_closed,
+                                                      t_neg);
                     }
                 } else if (active) {
                     const bool open_prev = ds_open(dsv);
@@ -1131,7 +1254,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     const bool can_sel = sel && D == 0 && !heavy;
                     Raw w0{}, w1{}, w2{}, w3{};
                     if (can_sel) {
-                        if (rstaged) {
+                        if (rstaged && !TINY) {
                             const Raw* rp = rules_s + (r0 - r_al);
                             if (nr > 0) w0 = rp[0];
                             if (nr > 1) w1 = rp[1];
@@ -1245,6 +1368,17 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 }
                 consumer_sync(kTileThreads);
             }
+            if (s.p2p && sel) {
+                // peer exchange: this tile's final P words (phase 2 + 3) straight
+                // into every peer's slot k % 3 -- NVLink stores that overlap the
+                // next tile's phases
+                const long long wb = (d0 + s.xbase) >> 5, we = (d0 + nd + s.xbase + 31) >> 5;
+                const int nw = (int)(we - wb);
+                for (int i = threadIdx.x; i < nw * s.world; i += kTileThreads) {
+                    const int r = i / nw, w = i - r * nw;
+                    if (r != s.rank) peer_slot(s, r, k % 3)[wb + w] = __ldcg(Pcur + wb + w);
+                }
+            }
         }
     }
 
@@ -1260,7 +1394,8 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     const bool bn = __syncthreads_or(t_neg);
     if (threadIdx.x == 0)
         finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0,
-                    s.x_stride ? Pcur + (long long)s.rank * s.x_stride + s.x_stride - 4 : nullptr);
+                    s.x_stride ? Pcur + (long long)s.rank * s.x_stride + s.x_stride - 4 : nullptr,
+                    s.p2p ? &s : nullptr);
 }
 
 // ---------------------------------------------------------------------------

@@ -76,11 +76,16 @@ struct snp_engine {
     int kind = RECV_PULL;
     bool tiled = false;
     long long p_words = 0;  // sharded: exchange words per P buffer
+    uint32_t* xblock = nullptr;            // sharded: exchange block (3 slots + step flags)
+    unsigned long long epoch = 0;          // runs begun (peer-exchange step flags)
+    std::vector<void*> ipc_opened;         // peer blocks mapped with cudaIpcOpenMemHandle
+    unsigned long long* d_peers = nullptr; // device array of every rank's block
     long long shard_lo = 0, shard_hi = 0, shard_nl = 0;
     cudaStream_t own_stream = nullptr;
     int step_block = kBlock;
     size_t step_smem = 0;
     bool wide_rules = false;
+    bool tiny_rules = false;  // tiled: 4-byte staged rule words (s.rw4)
     long long resident_ctas = 0;
     cudaStream_t stream = nullptr;
     std::vector<void*> allocs;
@@ -125,6 +130,7 @@ struct snp_engine {
     }
 
     ~snp_engine() {
+        for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
         if (graph) cudaGraphExecDestroy(graph);
         for (void* p : allocs) cudaFree(p);
         if (ev0) cudaEventDestroy(ev0);
@@ -207,7 +213,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
     cudaFuncAttributes fa{};
-    CU(cudaFuncGetAttributes(&fa, tiled_step_kernel<P_BIT, true, false, false>));
+    CU(cudaFuncGetAttributes(&fa, tiled_step_kernel<P_BIT, RW_WIDE, false, false>));
     const long long budget = (long long)smem_optin - (long long)fa.sharedSizeBytes - 128;
     auto acc_b = [&](long long t) { return 4ll * (e->acc16 ? acc_words<true>((int)t) : acc_words<false>((int)t)); };
     T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
@@ -266,12 +272,22 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
     }
+    // regular rule counts: offsets are implicit (rpn * local neuron)
+    s.rpn = 0;
+    if (q > 0) {
+        const long long r = roff_h[1] - roff_h[0];
+        bool regular = r >= 1 && r <= (long long)kLightRules;
+        for (long long i = 0; i < q && regular; ++i) regular = (long long)roff_h[i] == r * i;
+        regular = regular && (long long)roff_h[q] == r * q;
+        if (const char* env = getenv("SNPB200_RPN")) regular = regular && atoi(env) != 0;
+        if (regular) s.rpn = (int)r;
+    }
     // TMA stage descriptors (see tiled_step_kernel): phase-1 stages take as
     // many consecutive segments as fit with the P window they reference,
     // phase-2 stages kSub destinations with (when they fit) their rule words
     std::vector<StageDesc> desc;
     std::vector<uint32_t> tstage(n_tiles + 1, 0), sbases;
-    const uint32_t rw_size = e->wide_rules ? 16u : 8u;
+    const uint32_t rw_size = e->tiny_rules ? 4u : (e->wide_rules ? 16u : 8u);
     // P_BIT: stage the P-bit window of a stage's sources with its segments
     // (SNPB200_PSTAGE=0: look the bits up through L1/L2 instead)
     bool stage_p = e->p_mode == P_BIT;
@@ -305,8 +321,8 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         for (long long dd = 0; dd < nd; dd += kSub) {
             const uint32_t n = (uint32_t)std::min<long long>(kSub, nd - dd);
             const uint32_t rf = roff_h[d0 + dd], rl = roff_h[d0 + dd + n];
-            const uint32_t r_al = e->wide_rules ? rf : (rf & ~1u);
-            const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + r16((n + 1) * 4ull);
+            const uint32_t r_al = e->tiny_rules ? (rf & ~3u) : (e->wide_rules ? rf : (rf & ~1u));
+            const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + (s.rpn ? 0u : r16((n + 1) * 4ull));
             uint32_t rb = r16((unsigned long long)(rl - r_al) * rw_size);
             if (fixed + rb > kStageBytes) rb = 0;
             StageDesc sd;
@@ -346,15 +362,17 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
 // Build every device structure.  Host-side work is O(q + m + S) with plain
 // loops; the quadratic layouts (ELL pairs, dense rows) and the in-adjacency
 // transpose are built on the device.
+template <int PM, int RW>
+void pick_tiled_rw(snp_engine* e) {
+    e->step_fn = e->acc16 ? tiled_step_kernel<PM, RW, true, false> : tiled_step_kernel<PM, RW, false, false>;
+    e->lean_fn = e->acc16 ? tiled_step_kernel<PM, RW, true, true> : tiled_step_kernel<PM, RW, false, true>;
+}
+
 template <int PM>
 void pick_tiled(snp_engine* e) {
-    if (e->wide_rules) {
-        e->step_fn = e->acc16 ? tiled_step_kernel<PM, true, true, false> : tiled_step_kernel<PM, true, false, false>;
-        e->lean_fn = e->acc16 ? tiled_step_kernel<PM, true, true, true> : tiled_step_kernel<PM, true, false, true>;
-    } else {
-        e->step_fn = e->acc16 ? tiled_step_kernel<PM, false, true, false> : tiled_step_kernel<PM, false, false, false>;
-        e->lean_fn = e->acc16 ? tiled_step_kernel<PM, false, true, true> : tiled_step_kernel<PM, false, false, true>;
-    }
+    if (e->wide_rules) pick_tiled_rw<PM, RW_WIDE>(e);
+    else if (e->tiny_rules) pick_tiled_rw<PM, RW_TINY>(e);
+    else pick_tiled_rw<PM, RW_COMPACT>(e);
     e->prime_fn = prime_kernel<RECV_PULL, PM, true, false>;
 }
 
@@ -552,6 +570,23 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         TRY(upload(e, &d_rw, rw));
         s.rw = d_rw;
     }
+    // tiled: 4-byte rule words for the staged selection path when every rule
+    // fits (threshold, consumed < 2^10, produced < 2^4, delay < 2^7)
+    if (e->tiled && compact) {
+        bool tiny = true;
+        for (long long r = 0; r < m && tiny; ++r)
+            tiny = (rthr[r] & ~kExactBit) < 1024u && rrec[r].x < 1024 && rrec[r].y < 16 && rrec[r].z < 128;
+        if (const char* env = getenv("SNPB200_TINY")) tiny = tiny && atoi(env) != 0;
+        if (tiny) {
+            std::vector<uint32_t> rw4(m + 4);  // +4: 16-byte bulk-copy tails
+            for (long long r = 0; r < m; ++r)
+                rw4[r] = tiny_word(rthr[r], (uint32_t)rrec[r].x, (uint32_t)rrec[r].y, (uint32_t)rrec[r].z);
+            uint32_t* d_rw4;
+            TRY(upload(e, &d_rw4, rw4));
+            s.rw4 = d_rw4;
+            e->tiny_rules = true;
+        }
+    }
 
     uint32_t *d_soff = nullptr, *d_sdst = nullptr, *d_owner = nullptr;
     const bool need_owner = (e->format != SNP_FMT_COMPRESSED && have_adj);
@@ -683,7 +718,18 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             case P_U16: words = ceil_div(q + 1, 2) + 1; break;
             default: words = q + 2; break;
         }
-        for (int i = 0; i < 3; ++i) TRY(e->alloc(&st.P[i], words));
+        if (sh) {
+            // one exchange block: 3 slots, then `world` 64-bit step flags (peer
+            // exchange); a single allocation so it maps with one IPC handle
+            uint32_t* blk;
+            TRY(e->alloc(&blk, 3 * words + 2ll * sh->world + 2));
+            CU(cudaMemset(blk + 3 * words, 0, (2ll * sh->world + 2) * 4));
+            for (int i = 0; i < 3; ++i) st.P[i] = blk + i * words;
+            e->xblock = blk;
+            s.p_words = words;
+        } else {
+            for (int i = 0; i < 3; ++i) TRY(e->alloc(&st.P[i], words));
+        }
     } else {
         TRY(e->alloc(&st.recv, q));
         TRY(e->alloc(&st.list[0], q));
@@ -964,6 +1010,7 @@ int snp_begin(snp_engine* e, const int64_t* initial) {
     if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
     CU(cudaSetDevice(e->device));
     TRY(reset_state(e));
+    e->hctrl.epoch = ++e->epoch;
     const long long q = e->q;
     const long long* src = initial ? reinterpret_cast<const long long*>(initial) : e->initial.data();
     if (q > 0) CU(cudaMemcpyAsync(e->st.cfg, src, q * 8, cudaMemcpyHostToDevice, e->stream));
@@ -1343,6 +1390,69 @@ int snp_poll(snp_engine* e, snp_result* res) {
     fill_result(e, res);
     if (e->hctrl.halted && e->hctrl.reason == HALT_NEGATIVE)
         return fail(SNP_ERR_NEGATIVE, "spike counts went negative (row-partitioned run)");
+    if (e->hctrl.halted && e->hctrl.reason == HALT_EXCHANGE)
+        return fail(SNP_ERR_CUDA, "peer exchange timed out at step %lld (a rank stopped stepping)", e->hctrl.step);
+    return SNP_OK;
+}
+
+static int connect_peers(snp_engine* e, const std::vector<unsigned long long>& bases) {
+    DevSys& s = e->sys;
+    TRY(e->alloc(&e->d_peers, (long long)bases.size()));
+    CU(cudaMemcpy(e->d_peers, bases.data(), bases.size() * 8, cudaMemcpyHostToDevice));
+    s.peers = e->d_peers;
+    s.p2p = 1;
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    return SNP_OK;
+}
+
+int snp_exchange_ipc_handle(const snp_engine* e, void* handle) {
+    if (!e || !handle) return fail(SNP_ERR_BAD_ARG, "null argument");
+    if (!e->xblock) return fail(SNP_ERR_BAD_ARG, "not a row-partitioned engine");
+    CU(cudaSetDevice(e->device));
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, e->xblock));
+    memcpy(handle, &h, sizeof(h));
+    return SNP_OK;
+}
+
+int snp_exchange_connect(snp_engine* e, const void* handles, int world) {
+    if (!e || !handles) return fail(SNP_ERR_BAD_ARG, "null argument");
+    if (!e->xblock || world != e->sys.world) return fail(SNP_ERR_BAD_ARG, "world %d does not match the engine", world);
+    if (e->sys.p2p) return fail(SNP_ERR_BAD_ARG, "peer exchange already connected");
+    CU(cudaSetDevice(e->device));
+    std::vector<unsigned long long> bases(world);
+    for (int r = 0; r < world; ++r) {
+        if (r == e->sys.rank) {
+            bases[r] = (unsigned long long)e->xblock;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, static_cast<const char*>(handles) + (size_t)r * SNP_IPC_HANDLE_BYTES, sizeof(h));
+        void* p = nullptr;
+        CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        e->ipc_opened.push_back(p);
+        bases[r] = (unsigned long long)p;
+    }
+    return connect_peers(e, bases);
+}
+
+int snp_exchange_connect_local(snp_engine* const* engines, int world) {
+    if (!engines || world < 1) return fail(SNP_ERR_BAD_ARG, "null argument");
+    std::vector<unsigned long long> bases(world);
+    for (int r = 0; r < world; ++r) {
+        const snp_engine* x = engines[r];
+        if (!x || !x->xblock || x->sys.world != world || x->sys.rank != r)
+            return fail(SNP_ERR_BAD_ARG, "engine %d is not rank %d of a %d-way row partition", r, r, world);
+        bases[r] = (unsigned long long)x->xblock;
+    }
+    for (int r = 0; r < world; ++r) {
+        if (engines[r]->sys.p2p) return fail(SNP_ERR_BAD_ARG, "peer exchange already connected");
+        CU(cudaSetDevice(engines[r]->device));
+        TRY(connect_peers(engines[r], bases));
+    }
     return SNP_OK;
 }
 

@@ -345,6 +345,22 @@ class DeviceEngine:
         if rc:
             self._raise(rc)
 
+    def ipc_handle(self) -> bytes:
+        buf = nat.ctypes.create_string_buffer(nat.SNP_IPC_HANDLE_BYTES)
+        nat.check(self._lib.snp_exchange_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def connect_peers(self, handles: list[bytes]) -> None:
+        blob = b"".join(handles)
+        if len(blob) != nat.SNP_IPC_HANDLE_BYTES * len(handles):
+            raise ValueError("IPC handles must be SNP_IPC_HANDLE_BYTES each")
+        nat.check(self._lib.snp_exchange_connect(self._h, blob, len(handles)))
+
+    @staticmethod
+    def connect_local(engines: list["DeviceEngine"]) -> None:
+        arr = (nat.ctypes.c_void_p * len(engines))(*[e._h for e in engines])
+        nat.check(nat.load().snp_exchange_connect_local(arr, len(engines)))
+
     def launch_step(self) -> None:
         rc = self._lib.snp_launch_step(self._h)
         if rc:

@@ -127,17 +127,51 @@ class ShardedEngine:
             self._views = (full, chunk)
         return self._views
 
-    def run(self, max_steps: int, exchange: Callable[[int], None], selection: Selection = FirstApplicable(),
-            poll_every: int = 8, collect_stats: bool = False):
-        """Step to halt.  ``exchange(slot)`` must all-gather exchange slot
-        ``slot`` across ranks after each launch (same call on every rank)."""
+    # -- peer exchange (NVLink P2P, include/snpb200.h snp_exchange_connect) -----------
+
+    p2p = False
+
+    def ipc_handle(self) -> bytes:
+        """This rank's exchange block as a CUDA IPC handle (to all-gather)."""
+        return self.engine.ipc_handle()
+
+    def connect_p2p(self, handles: list[bytes]) -> None:
+        """Map every rank's exchange block (``handles[r]`` from rank r) and
+        switch to peer exchange: step kernels store their P chunk straight into
+        the peers' slots, so no per-step collective is called."""
+        self.engine.connect_peers(handles)
+        self.p2p = True
+
+    @staticmethod
+    def connect_local(shards: list["ShardedEngine"]) -> None:
+        """Peer exchange among ranks living in one process (tests: all ranks
+        on one device, stepped round-robin on one stream)."""
+        DeviceEngine.connect_local([s.engine for s in shards])
+        for s in shards:
+            s.p2p = True
+
+    def run(self, max_steps: int, exchange: Callable[[int], None] | None = None,
+            selection: Selection = FirstApplicable(), poll_every: int = 8, collect_stats: bool = False,
+            barrier: Callable[[], None] | None = None):
+        """Step to halt.  All-gather mode: ``exchange(slot)`` must all-gather
+        exchange slot ``slot`` across ranks after each launch (same call on
+        every rank).  Peer-exchange mode (after ``connect_p2p``): no exchange;
+        ``barrier()`` (a host barrier across ranks) runs after the reset so no
+        rank's first step lands in a peer that has not reset yet."""
+        if self.p2p and exchange is not None:
+            raise ValueError("peer exchange is connected: no per-step exchange callable")
+        if not self.p2p and exchange is None:
+            raise ValueError("all-gather mode needs an exchange callable")
         eng = self.engine
         eng.begin()
         eng.configure(max_steps, selection, collect_stats)
+        if barrier is not None:
+            barrier()
         k = 0
         while True:
             eng.launch_step()
-            exchange(k % 3)
+            if exchange is not None:
+                exchange(k % 3)
             k += 1
             if k % poll_every == 0 or k > max_steps:
                 res = eng.poll()
@@ -146,6 +180,22 @@ class ShardedEngine:
         cfg, dly = eng.read_state()
         reason = HaltReason.STEP_LIMIT if res.halt == nat.SNP_HALT_STEP_LIMIT else HaltReason.NO_APPLICABLE_RULES
         return cfg, dly, int(res.steps), reason, res.stats_dict(), k
+
+
+def torch_connect_p2p(sh: ShardedEngine, group=None) -> None:
+    """All-gather every rank's IPC handle over torch.distributed and connect
+    the peer exchange (one process per GPU, peers reachable over NVLink)."""
+    import torch.distributed as dist
+    handles: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, sh.ipc_handle(), group=group)
+    sh.connect_p2p(handles)
+    dist.barrier(group)
+
+
+def peer_access_ok(devices: list[int]) -> bool:
+    """Every pair of the given CUDA devices can map each other's memory."""
+    import torch
+    return all(a == b or torch.cuda.can_device_access_peer(a, b) for a in devices for b in devices)
 
 
 def torch_allgather_exchange(sh: ShardedEngine, group=None) -> Callable[[int], None]:
@@ -214,13 +264,20 @@ def synth_v1_rows(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_delays:
 
 def bench_sharded(args, rank: int, world: int) -> None:
     """Weak scaling: q = world x 10^7, each rank owns 10^7 rows; value is
-    whole-job 10^7-neuron-steps/s (= world x system steps/s)."""
+    whole-job 10^7-neuron-steps/s (= world x system steps/s).
+
+    Exchange: peer exchange (step kernels store P chunks straight into the
+    peers' slots over NVLink, no per-step collective) when every GPU pair can
+    map each other's memory, else the NCCL all-gather; SNPB200_EXCHANGE=nccl
+    forces the all-gather."""
     import json
     import os
     import time
 
     import torch
     import torch.distributed as dist
+
+    from bench import ClockSampler, algorithmic_bytes, measured_peaks
 
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local_rank)
@@ -232,42 +289,93 @@ def bench_sharded(args, rank: int, world: int) -> None:
     local = synth_v1_rows(q, lo, hi, with_delays=(args.workload == "k4"))
     gen_s = time.perf_counter() - t0
     sh = ShardedEngine(local, q, rank, world, device=local_rank)
-    ex = torch_allgather_exchange(sh)
+    ndev = torch.cuda.device_count()
+    use_p2p = os.environ.get("SNPB200_EXCHANGE", "p2p") != "nccl" and peer_access_ok(list(range(min(ndev, world))))
+    flag = torch.tensor([1 if use_p2p else 0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    use_p2p = bool(flag.item())
+    if use_p2p:
+        torch_connect_p2p(sh)
+        ex = None
+    else:
+        ex = torch_allgather_exchange(sh)
     sel = FirstApplicable()
     eng = sh.engine
-    eng.begin()
-    eng.configure(1 << 62, sel)
-    k = 0
-    for _ in range(args.warmup):
-        eng.launch_step()
-        ex(k % 3)
-        k += 1
+
+    def start_run(max_steps, initial=None, stats=False):
+        eng.begin(initial)
+        eng.configure(max_steps, sel, stats)
+        dist.barrier()  # peer exchange: every rank reset before any first step
+
+    def steps(n, k):
+        for _ in range(n):
+            eng.launch_step()
+            if ex is not None:
+                ex(k % 3)
+            k += 1
+        return k
+
+    start_run(1 << 62)
+    k = steps(args.warmup, 0)
     torch.cuda.synchronize()
     dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    for _ in range(args.steps):
-        eng.launch_step()
-        ex(k % 3)
-        k += 1
-    stop.record()
-    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record()
+        k = steps(args.steps, k)
+        stop.record()
+        torch.cuda.synchronize()
     ms = torch.tensor([start.elapsed_time(stop)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    dist.barrier()
     res = eng.poll()
+
+    # traffic counters of the same kind of steps (separate pass)
+    nk = min(args.steps, 30)
+    start_run(1 << 62, stats=True)
+    steps(args.warmup + nk, 0)
+    torch.cuda.synchronize()
+    st = eng.poll().stats_dict()
+    st = {kk: v * nk / max(1, args.warmup + nk) for kk, v in st.items()}
+    alg = algorithmic_bytes("compressed", hi - lo, 4 * (hi - lo), st, nk)
+
+    # e2e through the public API with host buffers: per step H2D of the rank's
+    # configuration, one step, D2H of the result (wall clock, max over ranks)
+    host = torch.from_numpy(local.initial.copy()).pin_memory()
+    e2e_n = max(3, min(args.steps, 10))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_n):
+        start_run(1, host.numpy())
+        steps(2, 0)
+        eng.poll()
+        cfg, _ = eng.read_state()
+        host.numpy()[:] = cfg
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    dist.barrier()
     if rank == 0:
         ms_step = ms.item() / args.steps
+        hbm = float(measured_peaks()["hbm_gbs"])
+        achieved = alg / (ms_step / 1000.0) / 1e9
+        xbytes = int(sh.x.slot_bytes) - int(sh.x.chunk_bytes)
         line = {
             "metric": "SNP steps/sec at 10^7 neurons", "value": world * 1000.0 / ms_step, "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (synth-v1 rows per rank)",
-            "config": {"workload": f"synth-v1 q={q} ({world} x 10^7), row-partitioned, NCCL all-gather of P bits",
+            "config": {"workload": f"synth-v1 q={q} ({world} x 10^7), row-partitioned",
+                       "exchange": "p2p (NVLink stores from the step kernel)" if use_p2p else "nccl all-gather",
                        "format": "compressed", "variant": "tiled", "policy": "first",
-                       "parallelism": f"rows/{world}", "exchange_bytes_per_step": int(sh.x.slot_bytes)},
+                       "parallelism": f"rows/{world}", "exchange_bytes_per_step": int(sh.x.slot_bytes),
+                       "l2": "working set >> 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "per": "GPU (rank 0's rows), whole step incl. exchange wait",
+                         "nvlink_GBps_in": xbytes / (ms_step / 1000.0) / 1e9},
+            "e2e": {"value": world * e2e_n / e2e_s.item(), "unit": "steps/s",
+                    "h2d_bytes_per_step": 8 * q, "d2h_bytes_per_step": 8 * q,
+                    "path": "ShardedEngine begin(host config) + 1 step + read_state, every rank"},
             "system_steps_per_s": 1000.0 / ms_step, "gpu_launches": args.steps, "halt": int(res.halt),
-            "setup_s": {"generate": gen_s},
+            "clocks": clk.summary(), "setup_s": {"generate": gen_s},
         }
         print(json.dumps(line))
     dist.destroy_process_group()

@@ -199,3 +199,104 @@ def test_sharded_engines_match_single(world, case):
     assert steps == want.steps
     if case == "sort":
         assert halt == 2 and cfg[600:].tolist() == list(range(1, 301))
+
+
+# -- GPU: peer exchange (P2P stores + step flags instead of the all-gather) -------------------
+
+def _run_p2p_on_one_gpu(arrays, world, max_steps, selection=snp.FirstApplicable()):
+    """All ranks in this process on cuda:0, connected with snp_exchange_connect_local
+    and stepped round-robin on one stream (so a rank's step-k flags are always set
+    before any rank's step k+1 waits for them)."""
+    q = arrays.neuron_count
+    L = shd.shard_layout(q, world)
+    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world) for r in range(world)]
+    shd.ShardedEngine.connect_local(ranks)
+    stream = torch.cuda.current_stream().cuda_stream
+    for r in ranks:
+        r.engine.set_stream(stream)
+    for run in range(2):  # a second run checks the per-run epoch of the step flags
+        for r in ranks:
+            r.engine.begin()
+            r.engine.configure(max_steps, selection)
+        k = 0
+        while True:
+            for r in ranks:
+                r.engine.launch_step()
+            k += 1
+            if k % 4 == 0 or k > max_steps:
+                res = [r.engine.poll() for r in ranks]
+                assert len({int(x.halt) for x in res}) == 1, "ranks disagree on halting"
+                if res[0].halt != 0:
+                    break
+    cfg = np.concatenate([r.engine.read_state()[0] for r in ranks])
+    dly = np.concatenate([r.engine.read_state()[1] for r in ranks])
+    return cfg, dly, int(res[0].steps), int(res[0].halt)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", ["synth", "synth_delays_seeded", "sort"])
+def test_peer_exchange_matches_single(world, case):
+    if case == "sort":
+        arrays = snp.sort_arrays(snp.SortInstance(300))
+        L, sel = 400, snp.FirstApplicable()
+    else:
+        arrays = snp.synth_v1(60_000, with_delays=case != "synth")
+        L = 12
+        sel = snp.SeededRandom(77) if "seeded" in case else snp.FirstApplicable()
+    want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED), snp.SimOptions(max_steps=L, selection=sel))
+    cfg, dly, steps, halt = _run_p2p_on_one_gpu(arrays, world, L, sel)
+    np.testing.assert_array_equal(cfg, want.config)
+    np.testing.assert_array_equal(dly, want.delays)
+    assert steps == want.steps
+    if case == "sort":
+        assert halt == 2 and cfg[600:].tolist() == list(range(1, 301))
+
+
+def _p2p_rank_proc(rank, world, q, steps, conn, out):
+    """One rank of a 2-process peer exchange on the same device (CUDA IPC)."""
+    import paper_2408_04343_b200 as snp_
+    from paper_2408_04343_b200 import sharded as shd_
+    arrays = snp_.synth_v1(q, with_delays=True)
+    L = shd_.shard_layout(q, world)
+    sh = shd_.ShardedEngine(shd_.local_arrays(arrays, L, rank), q, rank, world)
+    conn.send(sh.ipc_handle())
+    other = conn.recv()
+    handles = [None] * world
+    handles[rank], handles[1 - rank] = sh.ipc_handle(), other
+    sh.connect_p2p(handles)
+
+    def barrier():
+        conn.send("ready")
+        assert conn.recv() == "ready"
+
+    cfg, dly, nsteps, reason, _, _ = sh.run(steps, selection=snp_.SeededRandom(5), barrier=barrier)
+    out.put((rank, cfg, dly, nsteps))
+
+
+@pytest.mark.gpu
+def test_peer_exchange_two_processes_ipc():
+    """Two processes on one GPU mapping each other's exchange blocks through
+    CUDA IPC: the step flags and P stores cross a real process boundary and the
+    kernels wait on each other concurrently (time-sliced contexts)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q, steps = 40_000, 6
+    a, b = ctx.Pipe()
+    out = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_rank_proc, args=(r, 2, q, steps, c, out)) for r, c in ((0, a), (1, b))]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        r, cfg, dly, n = out.get(timeout=240)
+        got[r] = (cfg, dly, n)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    arrays = snp.synth_v1(q, with_delays=True)
+    want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED),
+                         snp.SimOptions(max_steps=steps, selection=snp.SeededRandom(5)))
+    np.testing.assert_array_equal(np.concatenate([got[0][0], got[1][0]]), want.config)
+    np.testing.assert_array_equal(np.concatenate([got[0][1], got[1][1]]), want.delays)
+    assert got[0][2] == got[1][2] == want.steps
