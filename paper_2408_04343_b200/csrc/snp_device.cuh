@@ -54,7 +54,10 @@ constexpr int kTileThreads = SNP_TILE_THREADS;  // consumer threads per CTA (mul
 static_assert(kTileThreads % 32 == 0 && kTileThreads + 32 <= 1024, "CTA must fit 1024 threads");
 constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
 constexpr uint32_t kDstBits = 15;         // destination slot within a tile
-constexpr uint32_t kSrcSpan = 1u << 17;   // source offset range within a segment
+constexpr uint32_t kSrcBits = 17;         // source offset within a segment
+constexpr uint32_t kSrcSpan = 1u << kSrcBits;
+constexpr uint32_t kSrcMask = kSrcSpan - 1u;
+static_assert(kDstBits + kSrcBits == 32, "segment words are 32 bits");
 constexpr uint32_t kDummyEdge = 0xffffffffu;  // CSR / legacy padding marker
 constexpr int kMaxTile = (1 << kDstBits) - 32;
 enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
@@ -117,8 +120,8 @@ struct DevSys {
     int ell_rows;             // z + 1
     long long p_common;       // P_BIT: the single produced amount
     // tiled pull (default COMPRESSED kernel)
-    const uint32_t* seg_words;  // [nseg * kSegEdges] (src - seg_base) << kDstBits | dst slot
-    const uint32_t* seg_base;   // [nseg] first source of each segment
+    const uint32_t* seg_words;  // [nseg * kSegEdges] dst slot << kSrcBits | (src - seg_base)
+    const uint32_t* seg_base;   // [nseg] first source of each segment, rounded down to 32
     const StageDesc* stages;    // TMA stage descriptors, tile-major (build_tiles)
     const uint32_t* tstage;     // [n_tiles + 1] stage range of each tile
     const uint32_t* stage_bases;  // segment bases per phase-1 stage (16-byte aligned runs)
@@ -127,6 +130,8 @@ struct DevSys {
     int tile;                   // destinations per tile (multiple of 32)
     int ring;                   // TMA ring stages (<= kMaxRing)
     int rpn;                    // tiled: rules per neuron when every neuron has the same count (<= 32), else 0
+    int pf;                     // tiled: ring stages prefetched into L2 ahead of the TMA copies (0 = off)
+    int dbg;                    // timing experiments (SNPB200_DEBUG_SKIP): 1 skip phase-1 math, 2 skip phase 2
     long long n_tiles;
     // row partition (sharded.py): local neuron j is global neuron gbase + j and
     // publishes its P bit at exchange-space position xbase + j; rank r's chunk
@@ -906,6 +911,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// L2 prefetch of a global range (no smem destination, no completion):
+// pulls a future ring stage's HBM bytes into L2 ahead of its TMA copy.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -922,7 +932,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 //
 // A CTA owns a tile of `s.tile` consecutive destinations.  Their in-edges are
 // stored sorted by source and cut into 256-edge segments whose sources span
-// < 2^17 (host build: build_tiles), each word = (src - seg_base) << 15 | slot.
+// < 2^17 (host build: build_tiles), each word = slot << 17 | (src - seg_base).
 // Warp-specialised: one producer warp streams everything the tile needs from
 // HBM through a kRingStages-deep TMA ring in shared memory (cp.async.bulk,
 // full/empty mbarriers); the consumer warps never wait on each other except
@@ -945,6 +955,11 @@ constexpr uint32_t kStageBytes = SNP_STAGE_KB * 1024u;  // one ring stage
 constexpr uint32_t kHdrBytes = 512;                     // stage header (+ segment bases)
 constexpr uint32_t kMaxSegPerStage = (kHdrBytes - 32) / 4;
 constexpr int kSub = kTileThreads;                      // destinations per phase-2 stage
+#ifndef SNP_SEG_SPLIT
+#define SNP_SEG_SPLIT 1
+#endif
+constexpr uint32_t kSegSplit = SNP_SEG_SPLIT;               // phase-1 work units per segment
+constexpr int kEpl = 8 / SNP_SEG_SPLIT;                      // edges per lane per work unit
 
 // Stage header, written by the producer thread with st.shared before the
 // mbarrier arrive (release), read by consumers after the wait (acquire).
@@ -965,6 +980,31 @@ static_assert(sizeof(StageHdr) <= kHdrBytes, "header fits");
 constexpr uint32_t kPayload = kHdrBytes;
 
 __device__ __forceinline__ uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
+
+// Phase-1 accumulation of one edge word (slot << 17 | offset) into the
+// tile's counters at shared address acc_s: 32-bit counters at slot * 4, or
+// 16-bit halves (word slot >> 1, half slot & 1).
+template <bool A16>
+__device__ __forceinline__ void tile_acc_add(uint32_t acc_s, uint32_t w, uint32_t v) {
+    if (A16) {
+        asm volatile(
+            "{\n.reg .b32 t, a, h, x;\n"
+            "and.b32 t, %0, 0xfffc0000;\n"
+            "shr.u32 t, t, 16;\n"
+            "add.u32 a, %1, t;\n"
+            "shr.u32 h, %0, 13;\n"
+            "and.b32 h, h, 16;\n"
+            "shl.b32 x, %2, h;\n"
+            "red.shared.add.u32 [a], x;\n}" ::"r"(w), "r"(acc_s), "r"(v) : "memory");
+    } else {
+        asm volatile(
+            "{\n.reg .b32 t, a;\n"
+            "and.b32 t, %0, 0xfffe0000;\n"
+            "shr.u32 t, t, 15;\n"
+            "add.u32 a, %1, t;\n"
+            "red.shared.add.u32 [a], %2;\n}" ::"r"(w), "r"(acc_s), "r"(v) : "memory");
+    }
+}
 
 // Shared 32-bit words holding the per-destination counters of a tile of T
 // destinations plus the dummy slot T that padding edges accumulate into.
@@ -1076,6 +1116,30 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
         uint32_t pround = 0;  // completed passes over the ring
         const uint32_t rw_size = TINY ? 4u : (WIDE ? 16u : 8u);
         const uint8_t* rw_src = TINY ? reinterpret_cast<const uint8_t*>(s.rw4) : reinterpret_cast<const uint8_t*>(s.rw);
+        // L2 prefetch cursor: s.pf stages ahead of the TMA ring, across this
+        // CTA's tiles, so the ring's copies hit L2 instead of waiting on HBM
+        long long pt = blockIdx.x;
+        uint32_t pi = 0, pe = 0;
+        if (pt < s.n_tiles) pi = __ldg(s.tstage + pt), pe = __ldg(s.tstage + pt + 1);
+        auto prefetch_next = [&]() {
+            if (pt >= s.n_tiles) return;
+            const uint4 da = __ldg(&s.stages[pi].a), db = __ldg(&s.stages[pi].b);
+            const uint32_t n = da.z;
+            if ((da.x & 0xff) == 1) {
+                if (n) bulk_prefetch_l2(s.seg_words + (size_t)da.y * kSegEdges, n * kSegEdges * 4u);
+            } else {
+                const long long j0 = pt * T + da.y;
+                bulk_prefetch_l2(st.cfg + j0, round16(n * 8u));
+                bulk_prefetch_l2(st.ds + j0, round16(n * 4u));
+                if (db.x) bulk_prefetch_l2(rw_src + (size_t)da.w * rw_size, db.x);
+            }
+            if (++pi == pe) {
+                pt += gridDim.x;
+                if (pt < s.n_tiles) pi = __ldg(s.tstage + pt), pe = __ldg(s.tstage + pt + 1);
+            }
+        };
+        if (lane == 0)
+            for (int i = 0; i < s.pf; ++i) prefetch_next();
         for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
             const long long d0 = tile * T;
             const uint32_t s0 = __ldg(s.tstage + tile), s1 = __ldg(s.tstage + tile + 1);
@@ -1092,6 +1156,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     for (uint32_t i = 0; i < cnt; ++i) {
                         const uint4 da = desc_s[i].a, db = desc_s[i].b;
                         const uint32_t kind = da.x, first = da.y, n = da.z, f3 = da.w, f4 = db.x, f5 = db.y;
+                        if (s.pf) prefetch_next();
                         const int b = pb;
                         if (pround > 0) mbar_wait(&empty_bar[b], (pround - 1) & 1u);
                         if (++pb == nst) {
@@ -1159,38 +1224,52 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 const uint32_t n = h->n, last = h->last, src0 = h->src0;
                 const bool pst = h->pstaged != 0;
                 const uint32_t* ps = reinterpret_cast<const uint32_t*>(buf + kPayload + n * kSegEdges * 4u);
-                for (uint32_t i = warp; i < n; i += kWarpsC) {
+                // work unit: 1/kSegSplit of a segment (kEpl edges per lane), so the
+                // stage's segments spread over all consumer warps
+                for (uint32_t c = warp; c < (s.dbg & 1 ? 0u : n * kSegSplit); c += kWarpsC) {
+                    const uint32_t i = c / kSegSplit, part = c % kSegSplit;
                     // lane l takes edges l, l+32, ...: each instruction covers 32
                     // consecutive (source-sorted) edges, so the P-bit loads hit
                     // nearly consecutive words -- conflict-free shared loads.
                     // Padding edges are (0, slot T): a real lookup into the
                     // dummy counter, so the loop has no branches.
                     const uint32_t base = h->bases[i];
-                    const uint32_t rel0 = base - src0;
-                    const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf + kPayload + i * kSegEdges * 4u) + lane;
-                    uint32_t w[8];
+                    const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf + kPayload + i * kSegEdges * 4u) +
+                                         part * (kSegEdges / kSegSplit) + lane;
+                    uint32_t w[kEpl];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) w[e] = wp[e * 32];
-                    auto add = [&](uint32_t we, uint32_t v) {
-                        const uint32_t slot = we & ((1u << kDstBits) - 1u);
-                        if (A16) atomicAdd(&acc[slot >> 1], v << ((slot & 1u) << 4));
-                        else atomicAdd(&acc[slot], v);
-                    };
+                    for (int e = 0; e < kEpl; ++e) w[e] = wp[e * 32];
+                    // word = slot << 17 | source offset.  Segment bases and src0 are
+                    // multiples of 32, so the offset's low 5 bits are the bit inside
+                    // its P word.  Addresses are a mask and a shifted add each
+                    // (LOP3 + LEA.HI, spelled in PTX so the pattern survives).
+                    const uint32_t acc_s = smem_u32(acc);
                     if (PM == P_BIT && pst) {
+                        const uint32_t pseg = smem_u32(ps) + ((base - src0) >> 3);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const uint32_t rel = rel0 + (w[e] >> kDstBits);
-                            add(w[e], (ps[rel >> 5] >> (rel & 31)) & 1u);  // src0 is a multiple of 128
+                        for (int e = 0; e < kEpl; ++e) {
+                            uint32_t v;
+                            asm volatile(
+                                "{\n.reg .b32 t, a, pw, r;\n"
+                                "and.b32 t, %1, %2;\n"
+                                "shr.u32 t, t, 3;\n"
+                                "add.u32 a, %3, t;\n"
+                                "ld.shared.u32 pw, [a];\n"
+                                "shf.r.wrap.b32 r, pw, pw, %1;\n"
+                                "and.b32 %0, r, 1;\n}"
+                                : "=r"(v) : "r"(w[e]), "n"(kSrcMask & ~31u), "r"(pseg) : "memory");
+                            tile_acc_add<A16>(acc_s, w[e], v);
                         }
                     } else {
                         // P looked up in global memory (L1/L2): non-bit P, or
                         // windows not staged
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) add(w[e], (uint32_t)p_lookup<PM>(Pprev, base + (w[e] >> kDstBits)));
+                        for (int e = 0; e < kEpl; ++e)
+                            tile_acc_add<A16>(acc_s, w[e], (uint32_t)p_lookup<PM>(Pprev, base + (w[e] & kSrcMask)));
                     }
                     if (stats_on) {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) stat[ST_EDGES] += ((w[e] & ((1u << kDstBits) - 1u)) != (uint32_t)T);
+                        for (int e = 0; e < kEpl; ++e) stat[ST_EDGES] += ((w[e] >> kSrcBits) != (uint32_t)T);
                     }
                 }
                 __syncwarp();
@@ -1235,7 +1314,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 const bool heavy = active && nr > kLightRules;
                 int r = -1;
                 long long pval = 0;
-                if (LEAN && !WIDE && rstaged && __all_sync(0xffffffffu, !active || nr <= 4u)) {
+                if (s.dbg & 2) {
+                    // timing experiment only: skip phase-2 work
+                } else if (LEAN && !WIDE && rstaged && __all_sync(0xffffffffu, !active || nr <= 4u)) {
                     // lean fast path: <= 4 staged rule words per neuron, branch-free selection
                     if (active) {
                         long long C = Cprev;
@@ -1383,6 +1464,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     }
 
     if (stats_on) flush_stats(ctl, stat);
+    if (s.dbg) t_fired = true;  // timing experiments: keep the run going
     const bool bf = __syncthreads_or(t_fired);
     const bool bc = __syncthreads_or(t_closed);
     __shared__ long long sh_neg_idx, sh_neg_val;

@@ -257,21 +257,27 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         unsigned long long e2 = start[t];
         const unsigned long long end = start[t + 1];
         while (e2 < end) {
-            const uint32_t b = bsrc[e2];
+            // bases are multiples of 32 so that an offset's low 5 bits index
+            // the bit inside a P word (tiled_step_kernel phase 1)
+            const uint32_t b = bsrc[e2] & ~31u;
             base.push_back(b);
             int n = 0;
             while (e2 < end && n < kSegEdges && bsrc[e2] - b < kSrcSpan) {
-                words.push_back(((bsrc[e2] - b) << kDstBits) | bslot[e2]);
+                words.push_back(((uint32_t)bslot[e2] << kSrcBits) | (bsrc[e2] - b));
                 ++e2;
                 ++n;
             }
             last.push_back(bsrc[e2 - 1]);
             // padding: source offset 0 (inside the window), dummy counter slot T
-            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T);
+            for (; n < kSegEdges; ++n) words.push_back((uint32_t)T << kSrcBits);
         }
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
     }
+    s.pf = 0;  // measured: L2 prefetch ahead of the ring does not help (profiles/r1_history.md)
+    if (const char* env = getenv("SNPB200_PREFETCH")) s.pf = std::max(0, atoi(env));
+    s.dbg = 0;
+    if (const char* env = getenv("SNPB200_DEBUG_SKIP")) s.dbg = atoi(env);
     // regular rule counts: offsets are implicit (rpn * local neuron)
     s.rpn = 0;
     if (q > 0) {
@@ -513,7 +519,17 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     // --- receive path and P width
     e->variant = d->variant;
     if (e->format == SNP_FMT_COMPRESSED) {
-        if (e->variant == SNP_VARIANT_AUTO) e->variant = SNP_VARIANT_TILED;
+        if (e->variant == SNP_VARIANT_AUTO) {
+            // tiled unless most rules sit in heavy-rule neurons (> 32 rules,
+            // e.g. the sorter's detectors): those select one warp per neuron
+            // in the tiled kernel but one CTA per neuron in the CSR pull kernel
+            long long heavy_rules = 0;
+            for (long long i = 0; i < q; ++i) {
+                const long long nr = d->offsets[i + 1] - d->offsets[i];
+                if (nr > (long long)kLightRules) heavy_rules += nr;
+            }
+            e->variant = (!sh && 2 * heavy_rules > m) ? SNP_VARIANT_PULL : SNP_VARIANT_TILED;
+        }
         e->kind = e->variant == SNP_VARIANT_PUSH ? RECV_ARRAY : RECV_PULL;
         e->tiled = e->variant == SNP_VARIANT_TILED;
     } else {
