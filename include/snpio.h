@@ -61,6 +61,11 @@ int snpio_write_file(const char *path, int64_t q, int64_t m, int64_t s, const in
                      const int64_t *consumed, const int64_t *produced, const int64_t *delay,
                      const int64_t *adj_offsets, const int64_t *adj_targets, int64_t output);
 
+/* format_trace (engine.py:162-165): `n_rows` configuration rows of q
+ * counts, one line each, space-separated; append = 1 adds to the file
+ * (a trace written segment by segment is byte-identical). */
+int snpio_write_trace(const char *path, const int64_t *rows, int64_t n_rows, int64_t q, int32_t append);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1225,8 +1225,12 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 const bool pst = h->pstaged != 0;
                 const uint32_t* ps = reinterpret_cast<const uint32_t*>(buf + kPayload + n * kSegEdges * 4u);
                 // work unit: 1/kSegSplit of a segment (kEpl edges per lane), so the
-                // stage's segments spread over all consumer warps
-                for (uint32_t c = warp; c < (s.dbg & 1 ? 0u : n * kSegSplit); c += kWarpsC) {
+                // stage's segments spread over all consumer warps.  A warp releases
+                // the stage as soon as its last unit's words and P bits are in
+                // registers; the shared atomics into the counters come after.
+                bool released = false;
+                const uint32_t units = (s.dbg & 1) ? 0u : n * kSegSplit;
+                for (uint32_t c = warp; c < units; c += kWarpsC) {
                     const uint32_t i = c / kSegSplit, part = c % kSegSplit;
                     // lane l takes edges l, l+32, ...: each instruction covers 32
                     // consecutive (source-sorted) edges, so the P-bit loads hit
@@ -1236,19 +1240,17 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     const uint32_t base = h->bases[i];
                     const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf + kPayload + i * kSegEdges * 4u) +
                                          part * (kSegEdges / kSegSplit) + lane;
-                    uint32_t w[kEpl];
+                    uint32_t w[kEpl], v[kEpl];
 #pragma unroll
                     for (int e = 0; e < kEpl; ++e) w[e] = wp[e * 32];
                     // word = slot << 17 | source offset.  Segment bases and src0 are
                     // multiples of 32, so the offset's low 5 bits are the bit inside
                     // its P word.  Addresses are a mask and a shifted add each
                     // (LOP3 + LEA.HI, spelled in PTX so the pattern survives).
-                    const uint32_t acc_s = smem_u32(acc);
                     if (PM == P_BIT && pst) {
                         const uint32_t pseg = smem_u32(ps) + ((base - src0) >> 3);
 #pragma unroll
                         for (int e = 0; e < kEpl; ++e) {
-                            uint32_t v;
                             asm volatile(
                                 "{\n.reg .b32 t, a, pw, r;\n"
                                 "and.b32 t, %1, %2;\n"
@@ -1257,23 +1259,31 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                                 "ld.shared.u32 pw, [a];\n"
                                 "shf.r.wrap.b32 r, pw, pw, %1;\n"
                                 "and.b32 %0, r, 1;\n}"
-                                : "=r"(v) : "r"(w[e]), "n"(kSrcMask & ~31u), "r"(pseg) : "memory");
-                            tile_acc_add<A16>(acc_s, w[e], v);
+                                : "=r"(v[e]) : "r"(w[e]), "n"(kSrcMask & ~31u), "r"(pseg) : "memory");
                         }
                     } else {
                         // P looked up in global memory (L1/L2): non-bit P, or
                         // windows not staged
 #pragma unroll
-                        for (int e = 0; e < kEpl; ++e)
-                            tile_acc_add<A16>(acc_s, w[e], (uint32_t)p_lookup<PM>(Pprev, base + (w[e] & kSrcMask)));
+                        for (int e = 0; e < kEpl; ++e) v[e] = (uint32_t)p_lookup<PM>(Pprev, base + (w[e] & kSrcMask));
                     }
+                    if (c + kWarpsC >= units) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty_bar[b]);
+                        released = true;
+                    }
+                    const uint32_t acc_s = smem_u32(acc);
+#pragma unroll
+                    for (int e = 0; e < kEpl; ++e) tile_acc_add<A16>(acc_s, w[e], v[e]);
                     if (stats_on) {
 #pragma unroll
                         for (int e = 0; e < kEpl; ++e) stat[ST_EDGES] += ((w[e] >> kSrcBits) != (uint32_t)T);
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[b]);
+                if (!released) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[b]);
+                }
                 if (last) break;
             }
             consumer_sync(kTileThreads);  // acc complete
@@ -1314,10 +1324,23 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 const bool heavy = active && nr > kLightRules;
                 int r = -1;
                 long long pval = 0;
+                bool released = false;
                 if (s.dbg & 2) {
                     // timing experiment only: skip phase-2 work
                 } else if (LEAN && !WIDE && rstaged && __all_sync(0xffffffffu, !active || nr <= 4u)) {
-                    // lean fast path: <= 4 staged rule words per neuron, branch-free selection
+                    // lean fast path: <= 4 staged rule words per neuron, branch-free
+                    // selection; the stage is released once they are in registers
+                    constexpr int kW = TINY ? 4 : 8;
+                    alignas(16) uint32_t wv[kW];
+                    if (active) {
+                        const uint32_t* rp = reinterpret_cast<const uint32_t*>(
+                            reinterpret_cast<const uint8_t*>(rules_s) + (r0 - r_al) * (TINY ? 4u : 8u));
+#pragma unroll
+                        for (int x = 0; x < kW; ++x) wv[x] = rp[x];
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[b]);
+                    released = true;
                     if (active) {
                         long long C = Cprev;
                         if (ds_open(dsv)) {
@@ -1325,8 +1348,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                             C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
                         }
                         const int D = ds_next(dsv);
-                        const uint8_t* rp = reinterpret_cast<const uint8_t*>(rules_s) + (r0 - r_al) * (TINY ? 4u : 8u);
-                        pval = lean_commit4<PM, TINY>(s, st, ctl, cx, j, nr, rp, C, D, sel && D == 0, t_fired, t_closed,
+                        pval = lean_commit4<PM, TINY>(s, st, ctl, cx, j, nr, wv, C, D, sel && D == 0, t_fired, t_closed,
                                                       t_neg);
                     }
                 } else if (active) {
@@ -1371,8 +1393,10 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                         }
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[b]);
+                if (!released) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[b]);
+                }
                 if (last) break;
             }
             consumer_sync(kTileThreads);  // phase-2 commits visible; acc free after phase 3

@@ -452,4 +452,30 @@ int snpio_write_file(const char* path, int64_t q, int64_t m, int64_t s, const in
     return ok ? SNPIO_OK : fail(SNPIO_ERR_IO, "write to %s failed", path);
 }
 
+int snpio_write_trace(const char* path, const int64_t* rows, int64_t n_rows, int64_t q, int32_t append) {
+    if (!path || n_rows < 0 || q < 0 || (n_rows && q && !rows)) return fail(SNPIO_ERR_IO, "bad arguments");
+    FILE* f = fopen(path, append ? "ab" : "wb");
+    if (!f) return fail(SNPIO_ERR_IO, "cannot open %s: %s", path, strerror(errno));
+    bool ok = true;
+    try {
+        Out o(f);
+        for (int64_t r = 0; ok && r < n_rows; ++r) {
+            const int64_t* row = rows + r * q;
+            for (int64_t i = 0; ok && i < q; ++i) {
+                ok = o.room(24);
+                if (i) o.put(' ');
+                o.num(row[i]);
+            }
+            ok = ok && o.room(2);
+            o.put('\n');
+        }
+        ok = ok && o.flush();
+    } catch (const std::bad_alloc&) {
+        fclose(f);
+        return fail(SNPIO_ERR_NOMEM, "out of host memory writing %s", path);
+    }
+    if (fclose(f) != 0) ok = false;
+    return ok ? SNPIO_OK : fail(SNPIO_ERR_IO, "write to %s failed", path);
+}
+
 }  // extern "C"

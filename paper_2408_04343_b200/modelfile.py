@@ -176,6 +176,7 @@ def _io_lib() -> ctypes.CDLL:
             "snpio_model_free": (None, [vp]),
             "snpio_write_file": (ctypes.c_int, [ctypes.c_char_p, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp,
                                                 vp, vp, i64]),
+            "snpio_write_trace": (ctypes.c_int, [ctypes.c_char_p, vp, i64, i64, ctypes.c_int32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -251,3 +252,14 @@ def save_model(path: str | os.PathLike, system) -> None:
     out = -1 if a.output_neuron is None else int(a.output_neuron)
     _check(_io_lib().snpio_write_file(os.fsencode(path), len(init), len(thr), len(adst),
                                       *map(_ptr, (init, off, thr, exact, cons, prod, dly, aoff, adst)), out))
+
+
+def write_trace(path: str | os.PathLike, trace, append: bool = False) -> None:
+    """Write ``format_trace(trace)`` to ``path`` with the native writer
+    (engine.py:162-165; byte-identical, without building the text in Python).
+    ``trace`` is a Trace or a sequence of configuration rows."""
+    rows = trace.configs if hasattr(trace, "configs") else trace
+    arr = np.ascontiguousarray(np.stack([np.asarray(r, dtype=np.int64) for r in rows]) if len(rows) else
+                               np.zeros((0, 0), np.int64))
+    q = arr.shape[1] if arr.ndim == 2 else 0
+    _check(_io_lib().snpio_write_trace(os.fsencode(path), _ptr(arr), arr.shape[0], q, 1 if append else 0))

@@ -92,3 +92,17 @@ def test_native_roundtrip_synthetic(tmp_path):
 def test_missing_file_is_oserror(tmp_path):
     with pytest.raises(OSError):
         mf.load_model(tmp_path / "nope.snp")
+
+
+def test_native_trace_writer_matches_format_trace(tmp_path):
+    rng = np.random.default_rng(3)
+    rows = [rng.integers(-5, 10**12, size=37) for _ in range(9)]
+    tr = snp.Trace(configs=rows, halt_reason=snp.HaltReason.STEP_LIMIT)
+    path = tmp_path / "t.trace"
+    mf.write_trace(path, tr)
+    assert path.read_text() == snp.format_trace(tr)
+    mf.write_trace(path, rows[:2], append=True)  # segment-by-segment writing
+    assert path.read_text() == snp.format_trace(tr) + "".join(" ".join(map(str, r)) + "\n" for r in rows[:2])
+    empty = snp.Trace(configs=[np.zeros(0, np.int64)] * 3, halt_reason=snp.HaltReason.STEP_LIMIT)
+    mf.write_trace(path, empty)
+    assert path.read_text() == snp.format_trace(empty) == "\n\n\n"
