@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SNPB200_ABI_VERSION 4
+#define SNPB200_ABI_VERSION 5
 
 enum {
     SNP_OK = 0,
@@ -56,6 +56,13 @@ enum { SNP_POLICY_FIRST = 0, SNP_POLICY_SEEDED = 1 };
 /* engine.py:57-60 RecordLevel as bit flags; 0 = final state only
  * (extension used by the benchmark). CONFIGS=1, CONFIGS_AND_DELAYS=3, FULL=7. */
 enum { SNP_REC_CONFIGS = 1, SNP_REC_DELAYS = 2, SNP_REC_SPIKING = 4 };
+/* Extension: with SNP_REC_DIGEST the recorded rows stay on the device and
+ * snp_advance returns one 64-bit digest per row instead (large recorded
+ * runs: 8 bytes per row instead of 8q).  digest(row) = sum over j of
+ * fmix64(v_j * 0x9E3779B97F4A7C15 + (j + 1) * 0xD6E8FEB86659FD93) mod 2^64,
+ * fmix64 the SplitMix64 finaliser of selection.py:37-45, v_j the int64 value
+ * (config count, delay, chosen rule id or -1). */
+enum { SNP_REC_DIGEST = 8 };
 
 /* engine.py:57-59 HaltReason */
 enum { SNP_RUNNING = 0, SNP_HALT_STEP_LIMIT = 1, SNP_HALT_NO_APPLICABLE = 2,
@@ -111,6 +118,9 @@ typedef struct snp_trace_out {
     int64_t first_row_step;  /* out: step of row 0 */
     int64_t config_rows;     /* out: rows of configs/delays written */
     int64_t spiking_rows;    /* out: rows of spiking written */
+    uint64_t *config_digests;  /* [cap] with SNP_REC_DIGEST (may be NULL) */
+    uint64_t *delay_digests;   /* [cap] */
+    uint64_t *spiking_digests; /* [cap] */
 } snp_trace_out;
 
 enum {

@@ -1673,6 +1673,28 @@ __global__ void update_delays_kernel(long long q, const int4* __restrict__ rrec,
 
 // Load (C, D) so that the next step kernel finalises exactly C_k = C, D_k = D
 // and then selects (sv_calc of engine.py:192-236).
+// Row digests for SNP_REC_DIGEST (include/snpb200.h): grid.y = row.
+__device__ __forceinline__ unsigned long long fmix64(unsigned long long z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+template <typename T>
+__global__ void __launch_bounds__(256) digest_rows_kernel(const T* __restrict__ rows, long long q,
+                                                          unsigned long long* out) {
+    const T* row = rows + (long long)blockIdx.y * q;
+    unsigned long long acc = 0;
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < q; j += (long long)gridDim.x * blockDim.x)
+        acc += fmix64((unsigned long long)(long long)row[j] * 0x9E3779B97F4A7C15ull +
+                      (unsigned long long)(j + 1) * 0xD6E8FEB86659FD93ull);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out + blockIdx.y, acc);
+}
+
 __global__ void load_state_kernel(long long q, long long* cfg, int* ds, const long long* __restrict__ C,
                                   const long long* __restrict__ D) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -110,6 +110,8 @@ struct snp_engine {
     long long tr_rows = 0;
     // phase scratch
     long long* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
+    unsigned long long* d_digest = nullptr;  // SNP_REC_DIGEST row digests (3 x digest_cap)
+    long long digest_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
 
@@ -909,7 +911,7 @@ int validate_opts(const snp_run_opts* o) {
     if (o->max_steps < 1) return fail(SNP_ERR_BAD_ARG, "max_steps must be >= 1, got %lld", (long long)o->max_steps);
     if (o->policy != SNP_POLICY_FIRST && o->policy != SNP_POLICY_SEEDED)
         return fail(SNP_ERR_BAD_ARG, "unknown policy %d", o->policy);
-    if (o->record & ~7) return fail(SNP_ERR_BAD_ARG, "bad record flags %d", o->record);
+    if (o->record & ~15) return fail(SNP_ERR_BAD_ARG, "bad record flags %d", o->record);
     return SNP_OK;
 }
 
@@ -1090,7 +1092,35 @@ int snp_advance(snp_engine* e, const snp_run_opts* o, int64_t n_steps, snp_trace
         long long cfg_rows = c.halted ? (k1 - k0 + 1) : (k1 - k0);
         long long sp_rows = k1 - k0;
         if (c.halted && c.reason == HALT_NEGATIVE) break;
-        if (record && cfg_rows > 0) {
+        if (record && (record & SNP_REC_DIGEST)) {
+            // digests only: one reduction per recorded row, 8 bytes back per row
+            if (e->digest_cap < chunk) {
+                TRY(e->alloc(&e->d_digest, 3 * chunk));
+                e->digest_cap = chunk;
+            }
+            CU(cudaMemsetAsync(e->d_digest, 0, 3 * chunk * 8, e->stream));
+            const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>(ceil_div(q, 256), 148));
+            const long long r0 = tr->config_rows, s0 = tr->spiking_rows;
+            if (cfg_rows > 0 && q > 0) {
+                if (record & REC_CONFIGS)
+                    digest_rows_kernel<long long><<<dim3(gx, (unsigned)cfg_rows), 256, 0, e->stream>>>(e->st.tr_cfg, q, e->d_digest);
+                if (record & REC_DELAYS)
+                    digest_rows_kernel<int><<<dim3(gx, (unsigned)cfg_rows), 256, 0, e->stream>>>(e->st.tr_dly, q, e->d_digest + chunk);
+            }
+            if (sp_rows > 0 && q > 0 && (record & REC_SPIKING))
+                digest_rows_kernel<int><<<dim3(gx, (unsigned)sp_rows), 256, 0, e->stream>>>(e->st.tr_chosen, q, e->d_digest + 2 * chunk);
+            CU(cudaGetLastError());
+            if (tr->config_digests && cfg_rows > 0)
+                CU(cudaMemcpyAsync(tr->config_digests + r0, e->d_digest, cfg_rows * 8, cudaMemcpyDeviceToHost, e->stream));
+            if (tr->delay_digests && cfg_rows > 0)
+                CU(cudaMemcpyAsync(tr->delay_digests + r0, e->d_digest + chunk, cfg_rows * 8, cudaMemcpyDeviceToHost, e->stream));
+            if (tr->spiking_digests && sp_rows > 0)
+                CU(cudaMemcpyAsync(tr->spiking_digests + s0, e->d_digest + 2 * chunk, sp_rows * 8, cudaMemcpyDeviceToHost,
+                                   e->stream));
+            CU(cudaStreamSynchronize(e->stream));
+            tr->config_rows += cfg_rows;
+            tr->spiking_rows += sp_rows;
+        } else if (record && cfg_rows > 0) {
             const long long r0 = tr->config_rows;
             if (tr->configs && (record & REC_CONFIGS))
                 CU(cudaMemcpy(tr->configs + r0 * q, e->st.tr_cfg, cfg_rows * q * 8, cudaMemcpyDeviceToHost));

@@ -298,6 +298,34 @@ class DeviceEngine:
         return Trace(configs=configs, halt_reason=reason,
                      delays=delays if want_d else None, spiking=spiking if want_s else None)
 
+    def trace_digests(self, options: SimOptions, initial: np.ndarray | None = None,
+                      rows_per_call: int = 1 << 16) -> "TraceDigests":
+        """``trace`` with the rows kept on the device: one 64-bit digest per
+        recorded row (``row_digest``) comes back instead of the row."""
+        flags = _REC_FLAGS[options.record] | nat.SNP_REC_DIGEST
+        self.begin(initial)
+        opts = self._opts(options.max_steps, options.selection, record=flags)
+        out = {"c": [], "d": [], "s": []}
+        res = nat.Result()
+        while True:
+            cap = rows_per_call
+            bufs = {k: np.zeros(cap, dtype=np.uint64) for k in out}
+            tr = nat.TraceOut()
+            tr.cap = cap
+            tr.config_digests, tr.delay_digests, tr.spiking_digests = (nat.ptr(bufs[k]) for k in ("c", "d", "s"))
+            rc = self._lib.snp_advance(self._h, nat.ctypes.byref(opts), cap, nat.ctypes.byref(tr), nat.ctypes.byref(res))
+            if rc:
+                self._raise(rc, res)
+            out["c"].append(bufs["c"][: tr.config_rows])
+            out["d"].append(bufs["d"][: tr.config_rows])
+            out["s"].append(bufs["s"][: tr.spiking_rows])
+            if res.halt != nat.SNP_RUNNING:
+                break
+        reason = HaltReason.STEP_LIMIT if res.halt == nat.SNP_HALT_STEP_LIMIT else HaltReason.NO_APPLICABLE_RULES
+        cat = {k: np.concatenate(v) for k, v in out.items()}
+        return TraceDigests(cat["c"], cat["d"] if flags & nat.SNP_REC_DELAYS else None,
+                            cat["s"] if flags & nat.SNP_REC_SPIKING else None, reason)
+
     def run_final(self, max_steps: int, selection: Selection = FirstApplicable(),
                   initial: np.ndarray | None = None, collect_stats: bool = False,
                   want_delays: bool = True) -> "RunResult":
@@ -480,6 +508,45 @@ def simulate(system, fmt: Format, options: SimOptions) -> Trace:
 
 def simulate_prepared(prep: Prepared, options: SimOptions) -> Trace:
     return prep.engine.trace(options)
+
+
+@dataclass(frozen=True)
+class TraceDigests:
+    """Per-row digests of a recorded run (``row_digest`` of ``configs[k]``,
+    ``delays[k]``, ``spiking[k]``); extension for runs too large to copy."""
+
+    configs: np.ndarray
+    delays: np.ndarray | None
+    spiking: np.ndarray | None
+    halt_reason: HaltReason
+
+    @property
+    def steps(self) -> int:
+        return len(self.configs) - 1
+
+
+_DIG_A, _DIG_B = np.uint64(0x9E3779B97F4A7C15), np.uint64(0xD6E8FEB86659FD93)
+
+
+def row_digest(row) -> int:
+    """Digest of one trace row (include/snpb200.h SNP_REC_DIGEST): the sum
+    over j of fmix64(v_j * A + (j + 1) * B) mod 2^64."""
+    v = np.asarray(row, dtype=np.int64).astype(np.uint64)
+    j = np.arange(1, v.size + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = v * _DIG_A + j * _DIG_B
+        z ^= z >> np.uint64(30)
+        z *= np.uint64(0xBF58476D1CE4E5B9)
+        z ^= z >> np.uint64(27)
+        z *= np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(31)
+    return int(z.sum(dtype=np.uint64))
+
+
+def trace_digests(prep: Prepared, options: SimOptions) -> TraceDigests:
+    """``simulate_prepared`` with every recorded row reduced to a 64-bit
+    digest on the device (8 bytes per row cross PCIe instead of 8q)."""
+    return prep.engine.trace_digests(options)
 
 
 def run_final(prep: Prepared, options: SimOptions, collect_stats: bool = False) -> RunResult:

@@ -140,3 +140,13 @@ def test_bench_csv(tmp_path, capsys):
     assert "build_ms" in capsys.readouterr().out
     assert run_cli("bench", "--family", "subsetsum", "--sizes", "3", "--formats", "compressed") == 0
     assert CSV_HEADER in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_run_digest_out_matches_trace(tmp_path):
+    trace = tmp_path / "t.trace"
+    digs = tmp_path / "t.dig"
+    assert run_cli("run", "--family", "sort", "-n", "12", "--format", "compressed", "--trace-out", str(trace)) == 0
+    assert run_cli("run", "--family", "sort", "-n", "12", "--format", "compressed", "--digest-out", str(digs)) == 0
+    rows = [[int(v) for v in line.split()] for line in trace.read_text().splitlines()]
+    assert digs.read_text().split() == [f"{snp.row_digest(r):016x}" for r in rows]

@@ -334,3 +334,36 @@ def test_trace_chunking_is_invisible():
     t2 = prep.engine.trace(opts)
     assert t1 == t2 and t1.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
     assert t1.configs[-1][600:].tolist() == list(range(1, 301))
+
+
+# -- device trace digests (SNP_REC_DIGEST) ------------------------------------------------
+
+@pytest.mark.parametrize("policy", ["first", "seeded7"])
+def test_trace_digests_match_rows(policy):
+    """Digests computed on the device equal row_digest of the recorded rows
+    (full trace of the same run) and of the C oracle's rows."""
+    a = snp.synth_v1(30_000, with_delays=True)
+    sel = POLICIES[policy]
+    prep = snp.prepare(a, snp.Format.COMPRESSED)
+    opts = snp.SimOptions(max_steps=25, selection=sel, record=snp.RecordLevel.FULL)
+    tr = snp.simulate_prepared(prep, opts)
+    dg = snp.trace_digests(prep, opts)
+    assert dg.halt_reason is tr.halt_reason and dg.steps == tr.steps
+    assert [int(x) for x in dg.configs] == [snp.row_digest(r) for r in tr.configs]
+    assert [int(x) for x in dg.delays] == [snp.row_digest(r) for r in tr.delays]
+    assert [int(x) for x in dg.spiking] == [snp.row_digest(r) for r in tr.spiking]
+    seed = 0 if policy == "first" else 7
+    ref, _, _ = coracle.run(OracleSystem.from_arrays(a), 25, 0 if policy == "first" else 1, seed, trace_rows=26)
+    assert [int(x) for x in dg.configs] == [snp.row_digest(r) for r in ref.configs]
+
+
+def test_trace_digests_sorter_halts():
+    a = snp.sort_arrays(snp.SortInstance(50))
+    for fmt, var in [(snp.Format.COMPRESSED, "tiled"), (snp.Format.ELL, "auto")]:
+        prep = snp.prepare(a, fmt, variant=var)
+        opts = snp.SimOptions(max_steps=200, record=snp.RecordLevel.CONFIGS)
+        dg = snp.trace_digests(prep, opts)
+        tr = snp.simulate_prepared(prep, opts)
+        assert dg.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES and dg.steps == tr.steps
+        assert [int(x) for x in dg.configs] == [snp.row_digest(r) for r in tr.configs]
+        assert dg.delays is None and dg.spiking is None
