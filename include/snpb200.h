@@ -244,6 +244,12 @@ int snp_exchange_ipc_handle(const snp_engine *eng, void *handle);
 int snp_exchange_connect(snp_engine *eng, const void *handles, int world);
 int snp_exchange_connect_local(snp_engine *const *engines, int world);
 
+/* Diagnostics: digests of the tiled layout arrays (segment words, segment
+ * bases, stage descriptors, tile->stage and tile->segment ranges, stage
+ * bases), row_digest-style sums; equal digests = identical layouts (the
+ * device build and the host reference build are checked this way). */
+int snp_engine_layout_digest(const snp_engine *eng, uint64_t *out /* [6] */);
+
 /* Timing helper for benchmarks: run `steps` steps (no recording) from the
  * current state with the device loop only and return the per-kernel mean
  * duration of the dominant step kernel in *kernel_ms (CUDA events around

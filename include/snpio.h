@@ -66,6 +66,16 @@ int snpio_write_file(const char *path, int64_t q, int64_t m, int64_t s, const in
  * (a trace written segment by segment is byte-identical). */
 int snpio_write_trace(const char *path, const int64_t *rows, int64_t n_rows, int64_t q, int32_t append);
 
+/* Synthetic family synth-v1 (paper_2408_04343_b200/generators.py synth_v1,
+ * SURVEY.md 8(d)), generated natively with all host threads: rows [lo, hi)
+ * (initial[n], offsets[n+1], 4 rules per neuron in [4n] arrays) and the CSR
+ * over all q sources of the edges entering [lo, hi) (ascending targets).
+ * snpio_synth_v1_edges gives the edge count to allocate. */
+int snpio_synth_v1_edges(int64_t q, uint64_t seed, int64_t lo, int64_t hi, int64_t *n_edges);
+int snpio_synth_v1(int64_t q, uint64_t seed, int32_t delays, int64_t lo, int64_t hi, int64_t *initial,
+                   int64_t *offsets, int64_t *threshold, uint8_t *is_exact, int64_t *consumed,
+                   int64_t *produced, int64_t *delay, int64_t *adj_offsets, int64_t *adj_targets);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,7 @@ SIGNATURES = [
     ("snp_configure", ctypes.c_int, [_EngineP, ctypes.POINTER(RunOpts)]),
     ("snp_launch_step", ctypes.c_int, [_EngineP]),
     ("snp_poll", ctypes.c_int, [_EngineP, ctypes.POINTER(Result)]),
+    ("snp_engine_layout_digest", ctypes.c_int, [_EngineP, ctypes.c_void_p]),
     ("snp_exchange_ipc_handle", ctypes.c_int, [_EngineP, ctypes.c_void_p]),
     ("snp_exchange_connect", ctypes.c_int, [_EngineP, ctypes.c_void_p, ctypes.c_int]),
     ("snp_exchange_connect_local", ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),

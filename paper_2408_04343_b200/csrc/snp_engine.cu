@@ -5,6 +5,7 @@
 // drives the per-step kernels of snp_device.cuh as CUDA-graph segments with
 // device-side halting; and implements the phase-level entry points.
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -14,6 +15,7 @@
 
 #include "../../include/snpb200.h"
 #include "snp_device.cuh"
+#include "snp_ingest.cuh"
 
 using namespace snp;
 
@@ -112,6 +114,7 @@ struct snp_engine {
     long long* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
     unsigned long long* d_digest = nullptr;  // SNP_REC_DIGEST row digests (3 x digest_cap)
     long long digest_cap = 0;
+    long long n_stages = 0, n_sbases = 0;   // tiled layout sizes (layout digest)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
 
@@ -176,9 +179,12 @@ struct ShardInput {
 // tiles of T; each tile's in-edges, visited in ascending source order (the
 // CSR out-adjacency is source-major, so a stable bucket pass keeps that
 // order), are packed into 256-edge segments whose sources span < 2^17.
+int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, long long S, bool stage_p);
+
 int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff_in,
                 const std::vector<uint32_t>& sdst_in, const std::vector<uint32_t>& roff_h,
-                std::vector<uint32_t>& heavy, const ShardInput* sh) {
+                std::vector<uint32_t>& heavy, const ShardInput* sh, const uint32_t* d_soff = nullptr,
+                const uint32_t* d_sdst = nullptr) {
     const std::vector<uint32_t>& soff = sh ? sh->soff : soff_in;
     const std::vector<uint32_t>& sdst = sh ? sh->sdst : sdst_in;
     const long long lo = sh ? sh->lo : 0, hi = sh ? sh->hi : e->q;
@@ -232,6 +238,38 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     const long long n_tiles = std::max<long long>(1, ceil_div(q, T));
     s.tile = (int)T;
     s.n_tiles = n_tiles;
+    s.pf = 0;  // measured: L2 prefetch ahead of the ring does not help (profiles/r1_history.md)
+    if (const char* env = getenv("SNPB200_PREFETCH")) s.pf = std::max(0, atoi(env));
+    s.dbg = 0;
+    if (const char* env = getenv("SNPB200_DEBUG_SKIP")) s.dbg = atoi(env);
+    // regular rule counts: offsets are implicit (rpn * local neuron)
+    s.rpn = 0;
+    if (q > 0) {
+        const long long r = roff_h[1] - roff_h[0];
+        bool regular = r >= 1 && r <= (long long)kLightRules;
+        for (long long i = 0; i < q && regular; ++i) regular = (long long)roff_h[i] == r * i;
+        regular = regular && (long long)roff_h[q] == r * q;
+        if (const char* env = getenv("SNPB200_RPN")) regular = regular && atoi(env) != 0;
+        if (regular) s.rpn = (int)r;
+    }
+    // P_BIT: stage the P-bit window of a stage's sources with its segments
+    // (SNPB200_PSTAGE=0: look the bits up through L1/L2 instead)
+    bool stage_p = e->p_mode == P_BIT;
+    if (const char* env = getenv("SNPB200_PSTAGE")) stage_p = stage_p && atoi(env) != 0;
+    // heavy-rule neurons per tile (heavy is ascending)
+    {
+        std::vector<uint32_t> theavy(n_tiles + 1, 0);
+        for (uint32_t hn : heavy) theavy[hn / T + 1]++;
+        for (long long t = 0; t < n_tiles; ++t) theavy[t + 1] += theavy[t];
+        uint32_t* d_theavy;
+        TRY(upload(e, &d_theavy, theavy));
+        s.theavy = d_theavy;
+    }
+    // the layout itself: on the device (default for a single engine with its
+    // out-adjacency on the device), or the host reference build below
+    bool dev_build = !sh && d_soff && d_sdst && sdst.size() < (1ull << 31);
+    if (const char* env = getenv("SNPB200_DEVICE_BUILD")) dev_build = dev_build && atoi(env) != 0;
+    if (dev_build) return build_tiles_device(e, d_soff, d_sdst, (long long)sdst.size(), stage_p);
     // bucket the edges into local destination tiles (source order preserved)
     std::vector<unsigned long long> start(n_tiles + 1, 0);
     for (size_t e2 = 0; e2 < sdst.size(); ++e2)
@@ -276,30 +314,12 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         tseg[t + 1] = (uint32_t)base.size();
         if (words.size() >= (1ull << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
     }
-    s.pf = 0;  // measured: L2 prefetch ahead of the ring does not help (profiles/r1_history.md)
-    if (const char* env = getenv("SNPB200_PREFETCH")) s.pf = std::max(0, atoi(env));
-    s.dbg = 0;
-    if (const char* env = getenv("SNPB200_DEBUG_SKIP")) s.dbg = atoi(env);
-    // regular rule counts: offsets are implicit (rpn * local neuron)
-    s.rpn = 0;
-    if (q > 0) {
-        const long long r = roff_h[1] - roff_h[0];
-        bool regular = r >= 1 && r <= (long long)kLightRules;
-        for (long long i = 0; i < q && regular; ++i) regular = (long long)roff_h[i] == r * i;
-        regular = regular && (long long)roff_h[q] == r * q;
-        if (const char* env = getenv("SNPB200_RPN")) regular = regular && atoi(env) != 0;
-        if (regular) s.rpn = (int)r;
-    }
     // TMA stage descriptors (see tiled_step_kernel): phase-1 stages take as
     // many consecutive segments as fit with the P window they reference,
     // phase-2 stages kSub destinations with (when they fit) their rule words
     std::vector<StageDesc> desc;
     std::vector<uint32_t> tstage(n_tiles + 1, 0), sbases;
     const uint32_t rw_size = e->tiny_rules ? 4u : (e->wide_rules ? 16u : 8u);
-    // P_BIT: stage the P-bit window of a stage's sources with its segments
-    // (SNPB200_PSTAGE=0: look the bits up through L1/L2 instead)
-    bool stage_p = e->p_mode == P_BIT;
-    if (const char* env = getenv("SNPB200_PSTAGE")) stage_p = stage_p && atoi(env) != 0;
     auto r16 = [](unsigned long long x) { return (uint32_t)((x + 15) & ~15ull); };
     for (long long t = 0; t < n_tiles; ++t) {
         uint32_t g = tseg[t];
@@ -349,21 +369,123 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     s.stages = d_desc;
     s.tstage = d_tstage;
     s.stage_bases = d_sbases;
+    e->n_stages = (long long)desc.size();
+    e->n_sbases = (long long)sbases.size();
 
-    // heavy-rule neurons per tile (heavy is ascending)
-    std::vector<uint32_t> theavy(n_tiles + 1, 0);
-    for (uint32_t hn : heavy) theavy[hn / T + 1]++;
-    for (long long t = 0; t < n_tiles; ++t) theavy[t + 1] += theavy[t];
-    uint32_t *d_words, *d_base, *d_tseg, *d_theavy;
+    uint32_t *d_words, *d_base, *d_tseg;
     TRY(upload(e, &d_words, words));
     TRY(upload(e, &d_base, base));
     TRY(upload(e, &d_tseg, tseg));
-    TRY(upload(e, &d_theavy, theavy));
     s.seg_words = d_words;
     s.seg_base = d_base;
     s.tseg = d_tseg;
-    s.theavy = d_theavy;
     e->in_edges = (long long)words.size();
+    return SNP_OK;
+}
+
+// Scratch device allocations freed at scope exit.
+struct TmpAllocs {
+    std::vector<void*> p;
+    ~TmpAllocs() {
+        for (void* x : p) cudaFree(x);
+    }
+    template <typename X>
+    cudaError_t get(X** out, long long n) {
+        void* v = nullptr;
+        cudaError_t err = cudaMalloc(&v, (size_t)std::max<long long>(n, 1) * sizeof(X));
+        if (err == cudaSuccess) p.push_back(v);
+        *out = static_cast<X*>(v);
+        return err;
+    }
+};
+
+// Device build of the same layout (snp_ingest.cuh).  Temporaries are freed
+// before returning; only the layout arrays stay with the engine.
+int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, long long S, bool stage_p) {
+    DevSys& s = e->sys;
+    const long long q = e->q, n_tiles = s.n_tiles;
+    const uint32_t T = (uint32_t)s.tile;
+    TmpAllocs tmp;
+    // 1-2: keys, stable sort by tile
+    uint32_t *k_in, *k_out;
+    unsigned long long *v_in, *v_out, *tstart;
+    CU(tmp.get(&k_in, S));
+    CU(tmp.get(&k_out, S));
+    CU(tmp.get(&v_in, S));
+    CU(tmp.get(&v_out, S));
+    CU(tmp.get(&tstart, n_tiles + 1));
+    if (q > 0) ingest_keys_kernel<<<grid_for(q), 256>>>(q, d_soff, d_sdst, T, k_in, v_in);
+    CU(cudaGetLastError());
+    int bits = 1;
+    while ((1ll << bits) <= n_tiles) ++bits;
+    size_t temp_bytes = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, k_in, k_out, v_in, v_out, (int)S, 0, bits));
+    void* temp;
+    CU(tmp.get(reinterpret_cast<unsigned char**>(&temp), (long long)temp_bytes));
+    if (S > 0) CU(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, (int)S, 0, bits));
+    ingest_tile_starts_kernel<<<grid_for(n_tiles + 1), 256>>>(S, k_out, n_tiles, tstart);
+    CU(cudaGetLastError());
+    // 3: segments (count, scan on the host, fill), words
+    const int wgrid = (int)std::max<long long>(1, std::min<long long>(ceil_div(n_tiles * 32, 256), 148ll * 8));
+    uint32_t* segc;
+    CU(tmp.get(&segc, n_tiles));
+    ingest_segments_kernel<<<wgrid, 256>>>(n_tiles, tstart, v_out, 0, segc, nullptr, nullptr, nullptr, nullptr, nullptr);
+    CU(cudaGetLastError());
+    std::vector<uint32_t> counts(n_tiles), tseg(n_tiles + 1, 0);
+    CU(cudaMemcpy(counts.data(), segc, n_tiles * 4, cudaMemcpyDeviceToHost));
+    for (long long t = 0; t < n_tiles; ++t) tseg[t + 1] = tseg[t] + counts[t];
+    const long long nseg = tseg[n_tiles];
+    if (nseg * (long long)kSegEdges >= (1ll << 32)) return fail(SNP_ERR_CAPACITY, "tiled layout exceeds 2^32 words");
+    uint32_t *d_tseg, *d_words, *d_base, *d_last, *d_segn;
+    unsigned long long* d_first;
+    TRY(upload(e, &d_tseg, tseg));
+    TRY(e->alloc(&d_words, nseg * kSegEdges));
+    TRY(e->alloc(&d_base, nseg));
+    CU(tmp.get(&d_last, nseg));
+    CU(tmp.get(&d_segn, nseg));
+    CU(tmp.get(&d_first, nseg));
+    ingest_segments_kernel<<<wgrid, 256>>>(n_tiles, tstart, v_out, 1, nullptr, d_tseg, d_first, d_segn, d_base, d_last);
+    CU(cudaGetLastError());
+    if (nseg > 0)
+        ingest_words_kernel<<<(int)std::min<long long>(ceil_div(nseg * 32, 256), 148ll * 64), 256>>>(
+            nseg, d_first, d_segn, d_base, v_out, T, d_words);
+    CU(cudaGetLastError());
+    // 4: stage descriptors (count, scan, fill)
+    IngestStageParams P{q, T, stage_p ? 1 : 0, s.rpn, e->tiny_rules ? 1 : 0, e->wide_rules ? 1 : 0, s.roff};
+    uint32_t *nst, *nsb;
+    CU(tmp.get(&nst, n_tiles));
+    CU(tmp.get(&nsb, n_tiles));
+    ingest_stages_kernel<<<wgrid, 256>>>(n_tiles, d_tseg, d_base, d_last, P, 0, nst, nsb, nullptr, nullptr, nullptr,
+                                         nullptr);
+    CU(cudaGetLastError());
+    std::vector<uint32_t> cst(n_tiles), csb(n_tiles), tstage(n_tiles + 1, 0), tsbase(n_tiles + 1, 0);
+    CU(cudaMemcpy(cst.data(), nst, n_tiles * 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(csb.data(), nsb, n_tiles * 4, cudaMemcpyDeviceToHost));
+    for (long long t = 0; t < n_tiles; ++t) {
+        tstage[t + 1] = tstage[t] + cst[t];
+        tsbase[t + 1] = tsbase[t] + csb[t];
+    }
+    uint32_t *d_tstage, *d_tsbase, *d_sbases;
+    StageDesc* d_desc;
+    TRY(upload(e, &d_tstage, tstage));
+    CU(tmp.get(&d_tsbase, n_tiles + 1));
+    CU(cudaMemcpy(d_tsbase, tsbase.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice));
+    TRY(e->alloc(&d_desc, tstage[n_tiles]));
+    TRY(e->alloc(&d_sbases, (long long)tsbase[n_tiles] + 4));
+    CU(cudaMemset(d_sbases, 0, ((size_t)tsbase[n_tiles] + 4) * 4));
+    ingest_stages_kernel<<<wgrid, 256>>>(n_tiles, d_tseg, d_base, d_last, P, 1, nullptr, nullptr, d_tstage, d_tsbase,
+                                         d_desc, d_sbases);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());
+    s.seg_words = d_words;
+    s.seg_base = d_base;
+    s.tseg = d_tseg;
+    s.stages = d_desc;
+    s.tstage = d_tstage;
+    s.stage_bases = d_sbases;
+    e->in_edges = nseg * kSegEdges;
+    e->n_stages = tstage[n_tiles];
+    e->n_sbases = (long long)tsbase[n_tiles] + 4;
     return SNP_OK;
 }
 
@@ -391,7 +513,22 @@ StepFn run_fn(const snp_engine* e) {
     return e->step_fn;
 }
 
+// SNPB200_TIMING=1: per-phase host timings of engine creation on stderr
+struct PhaseTimer {
+    bool on = getenv("SNPB200_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[snpb200 build] %-28s %8.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullptr) {
+    PhaseTimer tm;
     const long long q = d->q, m = d->m;
     if (q < 0 || m < 0) return fail(SNP_ERR_BAD_ARG, "q and m must be >= 0");
     if (q >= kInt32Max) return fail(SNP_ERR_CAPACITY, "q=%lld exceeds the int32 neuron index range", q);
@@ -438,6 +575,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         }
     }
 
+    tm.mark("rule vector");
     // --- transition structure
     std::vector<uint32_t> soff, sdst;
     bool have_adj = false;
@@ -518,6 +656,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     }
     e->z = z;
 
+    tm.mark("transition structure");
     // --- receive path and P width
     e->variant = d->variant;
     if (e->format == SNP_FMT_COMPRESSED) {
@@ -606,6 +745,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         }
     }
 
+    tm.mark("rule words");
     uint32_t *d_soff = nullptr, *d_sdst = nullptr, *d_owner = nullptr;
     const bool need_owner = (e->format != SNP_FMT_COMPRESSED && have_adj);
     if (have_adj) {
@@ -614,6 +754,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     }
     if (need_owner) TRY(upload(e, &d_owner, owner));
 
+    tm.mark("adjacency upload");
     // heavy list (CTA per neuron)
     std::vector<uint32_t> indeg;
     if (e->kind == RECV_PULL && !e->tiled && q > 0) {
@@ -658,7 +799,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     }
     if (sh && !(e->tiled && e->p_mode == P_BIT))
         return fail(SNP_ERR_BAD_ARG, "row partition needs COMPRESSED/tiled and one common produced amount (P bits)");
-    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, roff, heavy, sh));
+    tm.mark("in-adjacency / heavy");
+    if (e->tiled) TRY(build_tiles(e, d, soff, sdst, roff, heavy, sh, d_soff, d_sdst));
     uint32_t* d_heavy;
     TRY(upload(e, &d_heavy, heavy));
     s.heavy = d_heavy;
@@ -716,6 +858,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         e->dense_grid = dim3(col_tiles, splits, 1);
     }
 
+    tm.mark("tiled layout + formats");
     // --- run state
     TRY(e->alloc(&st.cfg, q + 8));  // +8: 16-byte bulk-copy tails
     TRY(e->alloc(&st.ds, q + 8));
@@ -757,6 +900,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     e->push_grid = grid_for(q);
     e->heavy_push_grid = 148 * 4;
 
+    tm.mark("run state");
     // kernel instances
     if (e->tiled) {
         switch (e->p_mode) {
@@ -1451,6 +1595,28 @@ static int connect_peers(snp_engine* e, const std::vector<unsigned long long>& b
         cudaGraphExecDestroy(e->graph);
         e->graph = nullptr;
     }
+    return SNP_OK;
+}
+
+int snp_engine_layout_digest(const snp_engine* e, uint64_t* out) {
+    if (!e || !out) return fail(SNP_ERR_BAD_ARG, "null argument");
+    memset(out, 0, 6 * sizeof(uint64_t));
+    if (!e->tiled) return SNP_OK;
+    CU(cudaSetDevice(e->device));
+    const DevSys& s = e->sys;
+    unsigned long long* d;
+    CU(cudaMalloc(&d, 6 * 8));
+    CU(cudaMemset(d, 0, 6 * 8));
+    const long long n[6] = {e->in_edges, e->in_edges / kSegEdges, e->n_stages * 8, s.n_tiles + 1, s.n_tiles + 1,
+                            e->n_sbases};
+    const uint32_t* a[6] = {s.seg_words, s.seg_base, reinterpret_cast<const uint32_t*>(s.stages), s.tstage, s.tseg,
+                            s.stage_bases};
+    for (int i = 0; i < 6; ++i)
+        if (n[i] > 0) digest_u32_kernel<<<grid_for(std::min<long long>(n[i], 148ll * 1024)), 256>>>(n[i], a[i], d + i);
+    cudaError_t err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaMemcpy(out, d, 6 * 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CU(err);
     return SNP_OK;
 }
 

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/snpio.h"
@@ -476,6 +477,140 @@ int snpio_write_trace(const char* path, const int64_t* rows, int64_t n_rows, int
     }
     if (fclose(f) != 0) ok = false;
     return ok ? SNPIO_OK : fail(SNPIO_ERR_IO, "write to %s failed", path);
+}
+
+}  // extern "C"
+
+// ---- synthetic family synth-v1 (generators.py synth_v1, synth_v1_rows)
+
+namespace {
+
+inline uint64_t mix64_h(uint64_t seed, int64_t stream, int64_t i) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(stream + 1) + 0xBF58476D1CE4E5B9ull * (uint64_t)(i + 1);
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+constexpr int kSynthDegree = 16;
+
+// the 16 ascending out-neighbours of source i
+inline void synth_targets(int64_t q, uint64_t seed, int64_t i, int64_t* t) {
+    const int64_t w = (q - 1) / kSynthDegree;
+    for (int k = 0; k < kSynthDegree; ++k)
+        t[k] = (i + 1 + k * w + (int64_t)(mix64_h(seed, 1 + k, i) % (uint64_t)w)) % q;
+    std::sort(t, t + kSynthDegree);
+}
+
+template <typename F>
+void parallel_for(int64_t n, F f) {
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>((int64_t)std::thread::hardware_concurrency(), n / 65536 + 1));
+    std::vector<std::thread> th;
+    for (int64_t t = 0; t < nt; ++t)
+        th.emplace_back([=] {
+            const int64_t a = n * t / nt, b = n * (t + 1) / nt;
+            f(a, b);
+        });
+    for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+int snpio_synth_v1_edges(int64_t q, uint64_t seed, int64_t lo, int64_t hi, int64_t* n_edges) {
+    if (q < kSynthDegree + 1 || lo < 0 || hi > q || lo > hi || !n_edges) return fail(SNPIO_ERR_IO, "bad arguments");
+    if (lo == 0 && hi == q) {
+        *n_edges = kSynthDegree * q;
+        return SNPIO_OK;
+    }
+    std::vector<int64_t> part(std::max<unsigned>(1, std::thread::hardware_concurrency()) + 1, 0);
+    const int64_t nt = (int64_t)part.size() - 1;
+    std::vector<std::thread> th;
+    for (int64_t t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            int64_t c = 0, tg[kSynthDegree];
+            for (int64_t i = q * t / nt; i < q * (t + 1) / nt; ++i) {
+                synth_targets(q, seed, i, tg);
+                for (int k = 0; k < kSynthDegree; ++k) c += tg[k] >= lo && tg[k] < hi;
+            }
+            part[t] = c;
+        });
+    for (auto& x : th) x.join();
+    int64_t tot = 0;
+    for (int64_t t = 0; t < nt; ++t) tot += part[t];
+    *n_edges = tot;
+    return SNPIO_OK;
+}
+
+int snpio_synth_v1(int64_t q, uint64_t seed, int32_t delays, int64_t lo, int64_t hi, int64_t* initial,
+                   int64_t* offsets, int64_t* threshold, uint8_t* is_exact, int64_t* consumed, int64_t* produced,
+                   int64_t* delay, int64_t* adj_offsets, int64_t* adj_targets) {
+    if (q < kSynthDegree + 1 || lo < 0 || hi > q || lo > hi) return fail(SNPIO_ERR_IO, "bad arguments");
+    const int64_t n = hi - lo;
+    // rows [lo, hi): initial spikes and the four rules (generators.py synth_v1)
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; ++r) {
+            const int64_t i = lo + r;
+            initial[r] = (int64_t)(mix64_h(seed, 0, i) % 8);
+            const int64_t t0 = 2 + (int64_t)(mix64_h(seed, 17, i) % 4), t1 = 3 + (int64_t)(mix64_h(seed, 18, i) % 6);
+            const int64_t c1 = 1 + (int64_t)(mix64_h(seed, 19, i) % (uint64_t)t1), t2 = 1 + (int64_t)(mix64_h(seed, 20, i) % 5);
+            const int64_t thr[4] = {t0, t1, t2, 1}, con[4] = {t0, c1, t2, 1}, pro[4] = {1, 1, 0, 1};
+            const uint8_t ex[4] = {1, 0, 1, 0};
+            int64_t dl[4] = {0, 0, 0, 0};
+            if (delays) {
+                dl[0] = (int64_t)(mix64_h(seed, 21, i) % 4);
+                dl[1] = (int64_t)(mix64_h(seed, 22, i) % 4);
+                dl[3] = (int64_t)(mix64_h(seed, 23, i) % 4);
+            }
+            for (int k = 0; k < 4; ++k) {
+                threshold[4 * r + k] = thr[k];
+                is_exact[4 * r + k] = ex[k];
+                consumed[4 * r + k] = con[k];
+                produced[4 * r + k] = pro[k];
+                delay[4 * r + k] = dl[k];
+            }
+            offsets[r] = 4 * r;
+        }
+    });
+    offsets[n] = 4 * n;
+    // adjacency over all q sources, edges entering [lo, hi), ascending targets
+    if (lo == 0 && hi == q) {
+        parallel_for(q, [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i) {
+                synth_targets(q, seed, i, adj_targets + kSynthDegree * i);
+                adj_offsets[i] = kSynthDegree * i;
+            }
+        });
+        adj_offsets[q] = kSynthDegree * q;
+        return SNPIO_OK;
+    }
+    std::vector<int64_t> cnt(q + 1, 0);
+    parallel_for(q, [&](int64_t a, int64_t b) {
+        int64_t tg[kSynthDegree];
+        for (int64_t i = a; i < b; ++i) {
+            synth_targets(q, seed, i, tg);
+            int64_t c = 0;
+            for (int k = 0; k < kSynthDegree; ++k) c += tg[k] >= lo && tg[k] < hi;
+            cnt[i] = c;
+        }
+    });
+    adj_offsets[0] = 0;
+    for (int64_t i = 0; i < q; ++i) adj_offsets[i + 1] = adj_offsets[i] + cnt[i];
+    parallel_for(q, [&](int64_t a, int64_t b) {
+        int64_t tg[kSynthDegree];
+        for (int64_t i = a; i < b; ++i) {
+            if (!cnt[i]) continue;
+            synth_targets(q, seed, i, tg);
+            int64_t w = adj_offsets[i];
+            for (int k = 0; k < kSynthDegree; ++k)
+                if (tg[k] >= lo && tg[k] < hi) adj_targets[w++] = tg[k];
+        }
+    });
+    return SNPIO_OK;
 }
 
 }  // extern "C"

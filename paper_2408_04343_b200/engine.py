@@ -373,6 +373,12 @@ class DeviceEngine:
         if rc:
             self._raise(rc)
 
+    def layout_digest(self) -> tuple[int, ...]:
+        """Digests of the tiled layout arrays (snp_engine_layout_digest)."""
+        out = np.zeros(6, dtype=np.uint64)
+        nat.check(self._lib.snp_engine_layout_digest(self._h, nat.ptr(out)))
+        return tuple(int(x) for x in out)
+
     def ipc_handle(self) -> bytes:
         buf = nat.ctypes.create_string_buffer(nat.SNP_IPC_HANDLE_BYTES)
         nat.check(self._lib.snp_exchange_ipc_handle(self._h, buf))

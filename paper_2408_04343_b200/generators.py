@@ -287,6 +287,35 @@ SYNTH_DEGREE = 16
 
 
 def synth_v1(q: int, seed: int = SYNTH_SEED, with_delays: bool = False) -> SystemArrays:
+    """The synthetic family below, generated natively with all host threads
+    (``snpio_synth_v1``; identical to :func:`synth_v1_numpy`)."""
+    if q < SYNTH_DEGREE + 1:
+        raise InvalidInstance(f"synth_v1 needs q >= {SYNTH_DEGREE + 1}, got {q}")
+    return synth_v1_native(q, 0, q, seed, with_delays)
+
+
+def synth_v1_native(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_delays: bool = False) -> SystemArrays:
+    """Rows [lo, hi) of synth_v1(q) and the CSR over all q sources of the edges
+    entering them (include/snpio.h snpio_synth_v1)."""
+    import ctypes
+
+    from .modelfile import _check, _io_lib, _ptr
+    lib = _io_lib()
+    seed_u = ctypes.c_uint64(seed & ((1 << 64) - 1))
+    ne = ctypes.c_int64()
+    _check(lib.snpio_synth_v1_edges(q, seed_u, lo, hi, ctypes.byref(ne)))
+    n, m = hi - lo, 4 * (hi - lo)
+    init, off = np.empty(n, np.int64), np.empty(n + 1, np.int64)
+    thr, cons, prod, dly = (np.empty(m, np.int64) for _ in range(4))
+    exact = np.empty(m, np.bool_)
+    aoff, adst = np.empty(q + 1, np.int64), np.empty(ne.value, np.int64)
+    _check(lib.snpio_synth_v1(q, seed_u, 1 if with_delays else 0, lo, hi,
+                              *map(_ptr, (init, off, thr, exact, cons, prod, dly, aoff, adst))))
+    owner = np.repeat(np.arange(n, dtype=np.int64), 4)
+    return SystemArrays(init, RuleVector(thr, exact, cons, prod, dly, owner), NeuronRuleMap(off), aoff, adst)
+
+
+def synth_v1_numpy(q: int, seed: int = SYNTH_SEED, with_delays: bool = False) -> SystemArrays:
     """Counter-based synthetic system: every quantity is ``mix64(seed,
     stream, neuron)`` so any shard can be rebuilt independently.
 

@@ -177,6 +177,8 @@ def _io_lib() -> ctypes.CDLL:
             "snpio_write_file": (ctypes.c_int, [ctypes.c_char_p, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp,
                                                 vp, vp, i64]),
             "snpio_write_trace": (ctypes.c_int, [ctypes.c_char_p, vp, i64, i64, ctypes.c_int32]),
+            "snpio_synth_v1_edges": (ctypes.c_int, [i64, ctypes.c_uint64, i64, i64, i64p]),
+            "snpio_synth_v1": (ctypes.c_int, [i64, ctypes.c_uint64, ctypes.c_int32, i64, i64] + [vp] * 9),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

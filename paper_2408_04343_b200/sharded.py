@@ -215,10 +215,17 @@ def torch_allgather_exchange(sh: ShardedEngine, group=None) -> Callable[[int], N
 
 # -- per-rank synthetic generation (weak-scaling bench) ------------------------------
 
-def synth_v1_rows(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_delays: bool = False,
-                  chunk: int = 4_000_000) -> SystemArrays:
+def synth_v1_rows(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_delays: bool = False) -> SystemArrays:
     """Rows [lo, hi) of ``synth_v1(q)`` plus every edge entering them, without
-    materialising the whole system (counter-based: any rank rebuilds its part)."""
+    materialising the whole system (counter-based: any rank rebuilds its part;
+    native, all host threads)."""
+    from .generators import synth_v1_native
+    return synth_v1_native(q, lo, hi, seed, with_delays)
+
+
+def synth_v1_rows_numpy(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_delays: bool = False,
+                        chunk: int = 4_000_000) -> SystemArrays:
+    """numpy restatement of :func:`synth_v1_rows` (cross-check)."""
     idx = np.arange(lo, hi, dtype=np.int64)
     n = hi - lo
 

@@ -367,3 +367,43 @@ def test_trace_digests_sorter_halts():
         assert dg.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES and dg.steps == tr.steps
         assert [int(x) for x in dg.configs] == [snp.row_digest(r) for r in tr.configs]
         assert dg.delays is None and dg.spiking is None
+
+
+# -- device-side ingest: the tiled layout built on the GPU == the host reference build ----------
+
+def _sparse_far_system(q=400_000, edges=50_000, seed=5):
+    """Few edges between far-apart neurons: segments cut by the 2^17 source-span rule."""
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, q, edges)
+    dst = rng.integers(0, q, edges)
+    keep = src != dst
+    pairs = np.unique(np.stack([src[keep], dst[keep]], axis=1), axis=0)
+    off = np.zeros(q + 1, np.int64)
+    np.cumsum(np.bincount(pairs[:, 0], minlength=q), out=off[1:])
+    base = snp.synth_v1(q)
+    return snp.SystemArrays(base.initial, base.rules, base.rule_map, off, pairs[:, 1].astype(np.int64))
+
+
+@pytest.mark.parametrize("case", ["synth", "synth_delays", "sort300", "sparse_far", "tiny"])
+def test_device_layout_build_matches_host(case, monkeypatch):
+    if case == "synth":
+        a = snp.synth_v1(700_000)
+    elif case == "synth_delays":
+        a = snp.synth_v1(123_457, with_delays=True)
+    elif case == "sort300":
+        a = snp.sort_arrays(snp.SortInstance(300))
+    elif case == "sparse_far":
+        a = _sparse_far_system()
+    else:
+        a = snp.synth_v1(17)
+    digests = []
+    finals = []
+    for dev in ("0", "1"):
+        monkeypatch.setenv("SNPB200_DEVICE_BUILD", dev)
+        prep = snp.prepare(a, snp.Format.COMPRESSED, variant="tiled")
+        digests.append(prep.engine.layout_digest())
+        finals.append(snp.run_final(prep, snp.SimOptions(max_steps=8, selection=snp.SeededRandom(4))).config)
+        del prep
+    assert digests[0] == digests[1]
+    assert any(digests[0])
+    np.testing.assert_array_equal(finals[0], finals[1])
