@@ -53,8 +53,11 @@ enum PMode { P_BIT = 0, P_U8 = 1, P_U16 = 2, P_U32 = 3 };
 constexpr int kTileThreads = SNP_TILE_THREADS;  // consumer threads per CTA (multiple of 32)
 static_assert(kTileThreads % 32 == 0 && kTileThreads + 32 <= 1024, "CTA must fit 1024 threads");
 constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
-constexpr uint32_t kDstBits = 15;         // destination slot within a tile
-constexpr uint32_t kSrcBits = 17;         // source offset within a segment
+#ifndef SNP_SRC_BITS
+#define SNP_SRC_BITS 16
+#endif
+constexpr uint32_t kSrcBits = SNP_SRC_BITS;  // source offset within a segment
+constexpr uint32_t kDstBits = 32 - kSrcBits; // destination slot within a tile
 constexpr uint32_t kSrcSpan = 1u << kSrcBits;
 constexpr uint32_t kSrcMask = kSrcSpan - 1u;
 static_assert(kDstBits + kSrcBits == 32, "segment words are 32 bits");
@@ -987,22 +990,25 @@ __device__ __forceinline__ uint32_t round16(uint32_t x) { return (x + 15u) & ~15
 template <bool A16>
 __device__ __forceinline__ void tile_acc_add(uint32_t acc_s, uint32_t w, uint32_t v) {
     if (A16) {
+        // word (slot >> 1) at byte (slot >> 1) * 4, half (slot & 1) * 16
         asm volatile(
             "{\n.reg .b32 t, a, h, x;\n"
-            "and.b32 t, %0, 0xfffc0000;\n"
-            "shr.u32 t, t, 16;\n"
+            "and.b32 t, %0, %3;\n"
+            "shr.u32 t, t, %4;\n"
             "add.u32 a, %1, t;\n"
-            "shr.u32 h, %0, 13;\n"
+            "shr.u32 h, %0, %5;\n"
             "and.b32 h, h, 16;\n"
             "shl.b32 x, %2, h;\n"
-            "red.shared.add.u32 [a], x;\n}" ::"r"(w), "r"(acc_s), "r"(v) : "memory");
+            "red.shared.add.u32 [a], x;\n}" ::"r"(w), "r"(acc_s), "r"(v), "n"(~((2u << kSrcBits) - 1u)),
+            "n"(kSrcBits - 1), "n"(kSrcBits - 4) : "memory");
     } else {
         asm volatile(
             "{\n.reg .b32 t, a;\n"
-            "and.b32 t, %0, 0xfffe0000;\n"
-            "shr.u32 t, t, 15;\n"
+            "and.b32 t, %0, %3;\n"
+            "shr.u32 t, t, %4;\n"
             "add.u32 a, %1, t;\n"
-            "red.shared.add.u32 [a], %2;\n}" ::"r"(w), "r"(acc_s), "r"(v) : "memory");
+            "red.shared.add.u32 [a], %2;\n}" ::"r"(w), "r"(acc_s), "r"(v), "n"(~((1u << kSrcBits) - 1u)),
+            "n"(kSrcBits - 2) : "memory");
     }
 }
 

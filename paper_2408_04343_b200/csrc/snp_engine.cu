@@ -11,6 +11,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/snpb200.h"
@@ -52,6 +53,24 @@ int fail(int code, const char* fmt, ...) {
 constexpr long long kInt32Max = 2147483647ll;
 
 inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+// Host loops over q / m / S run on all host threads (engine creation at 10^7+).
+// f(a, b) handles [a, b) and returns the first failing index there (or -1);
+// the smallest failing index over all chunks is returned, so errors are the
+// ones a sequential loop would report.
+template <typename F>
+long long parallel_first_fail(long long n, F f) {
+    const long long nt = std::max<long long>(
+        1, std::min<long long>((long long)std::max(1u, std::thread::hardware_concurrency()), n / (1 << 16) + 1));
+    if (nt == 1) return n > 0 ? f(0, n) : -1;
+    std::vector<long long> bad(nt, -1);
+    std::vector<std::thread> th;
+    for (long long t = 0; t < nt; ++t) th.emplace_back([&, t] { bad[t] = f(n * t / nt, n * (t + 1) / nt); });
+    for (auto& x : th) x.join();
+    for (long long b : bad)
+        if (b >= 0) return b;
+    return -1;
+}
 
 using StepFn = void (*)(DevSys, DevState);
 using PrimeFn = void (*)(DevSys, DevState, const long long*, const long long*, const long long*);
@@ -201,8 +220,20 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     // (P_BIT counts sending in-neighbours; other modes sum produced amounts)
     {
         std::vector<uint32_t> indeg(std::max<long long>(q, 1), 0);
-        for (size_t e2 = 0; e2 < sdst.size(); ++e2)
-            if ((long long)sdst[e2] >= lo && (long long)sdst[e2] < hi) indeg[sdst[e2] - lo]++;
+        if (!sh && d_sdst && !sdst.empty()) {
+            // in-degrees on the device (the adjacency is already there)
+            uint32_t* d_in;
+            CU(cudaMalloc(&d_in, (size_t)q * 4));
+            CU(cudaMemset(d_in, 0, (size_t)q * 4));
+            indeg_kernel<<<std::min(grid_for((long long)sdst.size()), 148 * 64), 256>>>((long long)sdst.size(), d_sdst, d_in);
+            cudaError_t err = cudaGetLastError();
+            if (err == cudaSuccess) err = cudaMemcpy(indeg.data(), d_in, (size_t)q * 4, cudaMemcpyDeviceToHost);
+            cudaFree(d_in);
+            CU(err);
+        } else {
+            for (size_t e2 = 0; e2 < sdst.size(); ++e2)
+                if ((long long)sdst[e2] >= lo && (long long)sdst[e2] < hi) indeg[sdst[e2] - lo]++;
+        }
         const long long unit = e->p_mode == P_BIT ? 1 : std::max<long long>(1, e->p_max);
         long long worst = 0;
         for (uint32_t x : indeg) worst = std::max<long long>(worst, (long long)x * unit);
@@ -210,9 +241,11 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         if (const char* env = getenv("SNPB200_ACC16")) e->acc16 = e->acc16 && atoi(env) != 0;
     }
     // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
-    // (3 tiles per SM with 16-bit counters leaves room for a 3 x 48 KB ring;
+    // (2 tiles per SM with 16-bit counters still leaves a 3 x 48 KB ring;
     // 4 per SM with 32-bit counters; measured on K3, profiles/r1_history.md)
-    long long T = ceil_div(std::max<long long>(q, 1), (e->acc16 ? 3ll : 4ll) * n_sm);
+    long long per_sm = e->acc16 ? 2 : 4;
+    if (const char* env = getenv("SNPB200_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
+    long long T = ceil_div(std::max<long long>(q, 1), per_sm * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
     if (const char* env = getenv("SNPB200_TILE")) T = atoll(env);
     // shared memory: the TMA ring (2..kMaxRing stages) plus the destination
@@ -225,6 +258,10 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     const long long budget = (long long)smem_optin - (long long)fa.sharedSizeBytes - 128;
     auto acc_b = [&](long long t) { return 4ll * (e->acc16 ? acc_words<true>((int)t) : acc_words<false>((int)t)); };
     T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
+    // large systems: cap T so that the ring keeps 3 stages
+    while (T > 32 * 64 && (budget - acc_b(T)) / (long long)kStageBytes < 3 &&
+           (budget - acc_b(T - 32)) / (long long)kStageBytes >= 1)
+        T -= 32;
     long long ring = std::min<long long>(kMaxRing, (budget - acc_b(T)) / (long long)kStageBytes);
     if (const char* env = getenv("SNPB200_RING")) ring = std::min<long long>(ring, atoll(env));
     if (ring < 2) {
@@ -547,31 +584,48 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     if (q > 0 && d->offsets[0] != 0) return fail(SNP_ERR_BAD_ARG, "offsets[0] must be 0");
     // +8 tail: the TMA stages of the tiled kernel copy whole 16-byte units
     std::vector<uint32_t> roff(q + 1 + 8, 0), owner(m);
-    for (long long i = 0; i < q; ++i) {
-        const long long a = d->offsets[i], b = d->offsets[i + 1];
-        if (b < a || b > m) return fail(SNP_ERR_BAD_ARG, "offsets not non-decreasing within [0, m]");
-        roff[i + 1] = (uint32_t)b;
-        for (long long r = a; r < b; ++r) owner[r] = (uint32_t)i;
-    }
+    if (parallel_first_fail(q, [&](long long a0, long long a1) -> long long {
+            for (long long i = a0; i < a1; ++i) {
+                const long long a = d->offsets[i], b = d->offsets[i + 1];
+                if (b < a || b > m) return i;
+                roff[i + 1] = (uint32_t)b;
+                for (long long r = a; r < b; ++r) owner[r] = (uint32_t)i;
+            }
+            return -1;
+        }) >= 0)
+        return fail(SNP_ERR_BAD_ARG, "offsets not non-decreasing within [0, m]");
     if ((q > 0 ? d->offsets[q] : 0) != m) return fail(SNP_ERR_BAD_ARG, "offsets[q] != m");
     std::vector<uint32_t> rthr(m);
     std::vector<int4> rrec(m);
+    const long long bad_rule = parallel_first_fail(m, [&](long long a, long long b) -> long long {
+        for (long long r = a; r < b; ++r) {
+            const long long t = d->threshold[r], c = d->consumed[r], p = d->produced[r], dl = d->delay[r];
+            if (t < 0 || t > kInt32Max || c < 0 || c > kInt32Max || p < 0 || p > kInt32Max || dl < 0 ||
+                dl > kInt32Max - 2)
+                return r;
+            rthr[r] = (uint32_t)t | (d->is_exact[r] ? kExactBit : 0u);
+            rrec[r] = make_int4((int)c, (int)p, (int)dl, 0);
+        }
+        return -1;
+    });
+    if (bad_rule >= 0) {
+        const long long r = bad_rule, t = d->threshold[r], dl = d->delay[r];
+        if (t < 0 || t > kInt32Max) return fail(SNP_ERR_CAPACITY, "rule %lld threshold %lld outside [0, 2^31-1]", r, t);
+        const long long c = d->consumed[r], p = d->produced[r];
+        if (c < 0 || c > kInt32Max || p < 0 || p > kInt32Max)
+            return fail(SNP_ERR_CAPACITY, "rule %lld consumed/produced outside [0, 2^31-1]", r);
+        return fail(SNP_ERR_CAPACITY, "rule %lld delay %lld outside [0, 2^31-3]", r, dl);
+    }
     bool compact = true;
     long long pmax = 0, pfirst = -1;
     bool pcommon = true;
     for (long long r = 0; r < m; ++r) {
-        const long long t = d->threshold[r], c = d->consumed[r], p = d->produced[r], dl = d->delay[r];
-        if (t < 0 || t > kInt32Max) return fail(SNP_ERR_CAPACITY, "rule %lld threshold %lld outside [0, 2^31-1]", r, t);
-        if (c < 0 || c > kInt32Max || p < 0 || p > kInt32Max)
-            return fail(SNP_ERR_CAPACITY, "rule %lld consumed/produced outside [0, 2^31-1]", r);
-        if (dl < 0 || dl > kInt32Max - 2) return fail(SNP_ERR_CAPACITY, "rule %lld delay %lld outside [0, 2^31-3]", r, dl);
-        rthr[r] = (uint32_t)t | (d->is_exact[r] ? kExactBit : 0u);
-        rrec[r] = make_int4((int)c, (int)p, (int)dl, 0);
-        if (c >= 65536 || p >= 256 || dl >= 256) compact = false;
-        if (p > 0) {
-            pmax = std::max(pmax, p);
-            if (pfirst < 0) pfirst = p;
-            else if (p != pfirst) pcommon = false;
+        const int4 x = rrec[r];
+        if (x.x >= 65536 || x.y >= 256 || x.z >= 256) compact = false;
+        if (x.y > 0) {
+            pmax = std::max<long long>(pmax, x.y);
+            if (pfirst < 0) pfirst = x.y;
+            else if (x.y != pfirst) pcommon = false;
         }
     }
 
@@ -585,11 +639,15 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         if (S >= (1ll << 32) - 1) return fail(SNP_ERR_CAPACITY, "synapse count %lld exceeds uint32", S);
         sdst.resize(S);
         for (long long i = 0; i <= q; ++i) soff[i] = (uint32_t)d->adj_offsets[i];
-        for (long long s = 0; s < S; ++s) {
-            const long long t = d->adj_targets[s];
-            if (t < 0 || t >= q) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", t);
-            sdst[s] = (uint32_t)t;
-        }
+        const long long bad = parallel_first_fail(S, [&](long long a, long long b) -> long long {
+            for (long long x = a; x < b; ++x) {
+                const long long t = d->adj_targets[x];
+                if (t < 0 || t >= q) return x;
+                sdst[x] = (uint32_t)t;
+            }
+            return -1;
+        });
+        if (bad >= 0) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", (long long)d->adj_targets[bad]);
         have_adj = true;
     } else if (d->syn_target && e->format == SNP_FMT_COMPRESSED) {
         // SynapseMatrix [rows][q]: the first NULL ends a column (matrices.py:100-112)
@@ -714,8 +772,11 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     e->wide_rules = !compact;
     if (compact) {
         std::vector<uint2> rw(m + 2);  // +2: 16-byte bulk-copy tails
-        for (long long r = 0; r < m; ++r)
-            rw[r] = make_uint2(rthr[r], (uint32_t)rrec[r].x | ((uint32_t)rrec[r].y << 16) | ((uint32_t)rrec[r].z << 24));
+        parallel_first_fail(m, [&](long long a, long long b) -> long long {
+            for (long long r = a; r < b; ++r)
+                rw[r] = make_uint2(rthr[r], (uint32_t)rrec[r].x | ((uint32_t)rrec[r].y << 16) | ((uint32_t)rrec[r].z << 24));
+            return -1;
+        });
         uint2* d_rw;
         TRY(upload(e, &d_rw, rw));
         s.rw = d_rw;
@@ -730,14 +791,19 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     // tiled: 4-byte rule words for the staged selection path when every rule
     // fits (threshold, consumed < 2^10, produced < 2^4, delay < 2^7)
     if (e->tiled && compact) {
-        bool tiny = true;
-        for (long long r = 0; r < m && tiny; ++r)
-            tiny = (rthr[r] & ~kExactBit) < 1024u && rrec[r].x < 1024 && rrec[r].y < 16 && rrec[r].z < 128;
+        bool tiny = parallel_first_fail(m, [&](long long a, long long b) -> long long {
+            for (long long r = a; r < b; ++r)
+                if (!((rthr[r] & ~kExactBit) < 1024u && rrec[r].x < 1024 && rrec[r].y < 16 && rrec[r].z < 128)) return r;
+            return -1;
+        }) < 0;
         if (const char* env = getenv("SNPB200_TINY")) tiny = tiny && atoi(env) != 0;
         if (tiny) {
             std::vector<uint32_t> rw4(m + 4);  // +4: 16-byte bulk-copy tails
-            for (long long r = 0; r < m; ++r)
-                rw4[r] = tiny_word(rthr[r], (uint32_t)rrec[r].x, (uint32_t)rrec[r].y, (uint32_t)rrec[r].z);
+            parallel_first_fail(m, [&](long long a, long long b) -> long long {
+                for (long long r = a; r < b; ++r)
+                    rw4[r] = tiny_word(rthr[r], (uint32_t)rrec[r].x, (uint32_t)rrec[r].y, (uint32_t)rrec[r].z);
+                return -1;
+            });
             uint32_t* d_rw4;
             TRY(upload(e, &d_rw4, rw4));
             s.rw4 = d_rw4;
