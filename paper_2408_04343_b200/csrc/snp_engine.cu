@@ -243,7 +243,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
     // (2 tiles per SM with 16-bit counters still leaves a 3 x 48 KB ring;
     // 4 per SM with 32-bit counters; measured on K3, profiles/r1_history.md)
-    long long per_sm = e->acc16 ? 2 : 4;
+    long long per_sm = (e->acc16 && heavy.empty()) ? 2 : 4;  // heavy-rule systems: more, smaller tiles
     if (const char* env = getenv("SNPB200_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
     long long T = ceil_div(std::max<long long>(q, 1), per_sm * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
