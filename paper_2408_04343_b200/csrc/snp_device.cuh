@@ -552,6 +552,14 @@ __device__ __forceinline__ long long light_commit(const DevSys& s, const DevStat
     return pval;
 }
 
+// x mod c for c in 1..4 (choose_index, selection.py:66-71) without a 64-bit
+// division: 2^32 = 1 (mod 3), so x mod 3 = (hi mod 3 + lo mod 3) mod 3.
+__device__ __forceinline__ uint32_t mod_upto4(unsigned long long x, uint32_t c) {
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    if (c == 3) return (hi % 3u + lo % 3u) % 3u;
+    return lo & (c - 1u);  // c = 1, 2, 4
+}
+
 // Lean light-neuron tail (no recording, no counters) for <= 4 compact rule
 // words already in shared memory: the same decisions as light_commit, computed
 // branch-free on a 32-bit saturated count (thresholds are < 2^31).  A negative
@@ -596,7 +604,7 @@ __device__ __forceinline__ long long lean_commit4(const DevSys& s, const DevStat
     if (cx.policy == 0) {
         idx = __ffs(mask) - 1;
     } else {
-        idx = mask ? nth_set_bit(mask, (uint32_t)(mix64(cx.seed, cx.k, j + s.gbase) % (uint32_t)__popc(mask))) : 0;
+        idx = mask ? nth_set_bit(mask, mod_upto4(mix64(cx.seed, cx.k, j + s.gbase), (uint32_t)__popc(mask))) : 0;
     }
     uint32_t c, p, d;
     if (TINY) {

@@ -204,7 +204,10 @@ def torch_allgather_exchange(sh: ShardedEngine, group=None) -> Callable[[int], N
     after the step kernel without a host sync."""
     import torch
     import torch.distributed as dist
-    sh.engine.set_stream(torch.cuda.current_stream().cuda_stream)
+    cur = torch.cuda.current_stream()
+    if cur.cuda_stream == 0:
+        raise ValueError("make a non-default stream current first (the engine cannot launch on the legacy stream)")
+    sh.engine.set_stream(cur.cuda_stream)
     full, chunk = sh.slots_torch()
 
     def exchange(slot: int) -> None:
@@ -287,18 +290,34 @@ def bench_sharded(args, rank: int, world: int) -> None:
     from bench import ClockSampler, algorithmic_bytes, measured_peaks
 
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # SNPB200_BENCH_SAME_DEVICE=1 (testing the script on a 1-GPU box): every
+    # rank on cuda:0, host collectives over gloo, peer exchange through IPC
+    same_dev = os.environ.get("SNPB200_BENCH_SAME_DEVICE") == "1"
+    dev = 0 if same_dev else local_rank
+    torch.cuda.set_device(dev)
+    if same_dev:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    cdev = "cpu" if same_dev else "cuda"  # device of the collectives' tensors
     q = args.q * world
     layout = shard_layout(q, world)
     lo, hi = layout.bounds(rank)
     t0 = time.perf_counter()
     local = synth_v1_rows(q, lo, hi, with_delays=(args.workload == "k4"))
     gen_s = time.perf_counter() - t0
-    sh = ShardedEngine(local, q, rank, world, device=local_rank)
+    sh = ShardedEngine(local, q, rank, world, device=dev)
     ndev = torch.cuda.device_count()
-    use_p2p = os.environ.get("SNPB200_EXCHANGE", "p2p") != "nccl" and peer_access_ok(list(range(min(ndev, world))))
-    flag = torch.tensor([1 if use_p2p else 0], device="cuda")
+    use_p2p = same_dev or (os.environ.get("SNPB200_EXCHANGE", "p2p") != "nccl" and
+                           peer_access_ok(list(range(min(ndev, world)))))
+    # the engine launches on a dedicated (non-default) torch stream that is
+    # also torch's current stream: the CUDA events below and the all-gather
+    # are ordered with its kernels (the legacy default stream would not be:
+    # snp_set_stream(NULL) means the engine's own non-blocking stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sh.engine.set_stream(stream.cuda_stream)
+    flag = torch.tensor([1 if use_p2p else 0], device=cdev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     use_p2p = bool(flag.item())
     if use_p2p:
@@ -327,12 +346,12 @@ def bench_sharded(args, rank: int, world: int) -> None:
     torch.cuda.synchronize()
     dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev) as clk:
         start.record()
         k = steps(args.steps, k)
         stop.record()
         torch.cuda.synchronize()
-    ms = torch.tensor([start.elapsed_time(stop)], device="cuda")
+    ms = torch.tensor([start.elapsed_time(stop)], device=cdev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     res = eng.poll()
 
@@ -357,7 +376,7 @@ def bench_sharded(args, rank: int, world: int) -> None:
         eng.poll()
         cfg, _ = eng.read_state()
         host.numpy()[:] = cfg
-    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=cdev)
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     dist.barrier()
     if rank == 0:

@@ -211,9 +211,9 @@ def _run_p2p_on_one_gpu(arrays, world, max_steps, selection=snp.FirstApplicable(
     L = shd.shard_layout(q, world)
     ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world) for r in range(world)]
     shd.ShardedEngine.connect_local(ranks)
-    stream = torch.cuda.current_stream().cuda_stream
+    stream = torch.cuda.Stream()  # one non-default stream: strictly round-robin execution
     for r in ranks:
-        r.engine.set_stream(stream)
+        r.engine.set_stream(stream.cuda_stream)
     for run in range(2):  # a second run checks the per-run epoch of the step flags
         for r in ranks:
             r.engine.begin()
