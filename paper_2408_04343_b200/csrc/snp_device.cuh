@@ -995,9 +995,9 @@ __device__ __forceinline__ uint32_t round16(uint32_t x) { return (x + 15u) & ~15
 // Phase-1 accumulation of one edge word (slot << 17 | offset) into the
 // tile's counters at shared address acc_s: 32-bit counters at slot * 4, or
 // 16-bit halves (word slot >> 1, half slot & 1).
-template <bool A16>
+template <int CB>
 __device__ __forceinline__ void tile_acc_add(uint32_t acc_s, uint32_t w, uint32_t v) {
-    if (A16) {
+    if (CB == 16) {
         // word (slot >> 1) at byte (slot >> 1) * 4, half (slot & 1) * 16
         asm volatile(
             "{\n.reg .b32 t, a, h, x;\n"
@@ -1009,6 +1009,18 @@ __device__ __forceinline__ void tile_acc_add(uint32_t acc_s, uint32_t w, uint32_
             "shl.b32 x, %2, h;\n"
             "red.shared.add.u32 [a], x;\n}" ::"r"(w), "r"(acc_s), "r"(v), "n"(~((2u << kSrcBits) - 1u)),
             "n"(kSrcBits - 1), "n"(kSrcBits - 4) : "memory");
+    } else if (CB == 8) {
+        // word (slot >> 2) at byte (slot >> 2) * 4, byte (slot & 3) * 8
+        asm volatile(
+            "{\n.reg .b32 t, a, h, x;\n"
+            "and.b32 t, %0, %3;\n"
+            "shr.u32 t, t, %4;\n"
+            "add.u32 a, %1, t;\n"
+            "shr.u32 h, %0, %5;\n"
+            "and.b32 h, h, 24;\n"
+            "shl.b32 x, %2, h;\n"
+            "red.shared.add.u32 [a], x;\n}" ::"r"(w), "r"(acc_s), "r"(v), "n"(~((4u << kSrcBits) - 1u)),
+            "n"(kSrcBits), "n"(kSrcBits - 3) : "memory");
     } else {
         asm volatile(
             "{\n.reg .b32 t, a;\n"
@@ -1020,10 +1032,18 @@ __device__ __forceinline__ void tile_acc_add(uint32_t acc_s, uint32_t w, uint32_
     }
 }
 
+// Counter of destination i (phase 2).
+template <int CB>
+__device__ __forceinline__ uint32_t tile_acc_get(const uint32_t* acc, int i) {
+    if (CB == 16) return (acc[i >> 1] >> ((i & 1) << 4)) & 0xffffu;
+    if (CB == 8) return (acc[i >> 2] >> ((i & 3) << 3)) & 0xffu;
+    return acc[i];
+}
+
 // Shared 32-bit words holding the per-destination counters of a tile of T
 // destinations plus the dummy slot T that padding edges accumulate into.
-template <bool A16>
-__host__ __device__ constexpr int acc_words(int T) { return A16 ? (T + 2) / 2 : T + 1; }
+template <int CB>
+__host__ __device__ constexpr int acc_words(int T) { return CB == 8 ? (T + 4) / 4 : (CB == 16 ? (T + 2) / 2 : T + 1); }
 
 // Stage descriptor (built on the host, build_tiles): 32 bytes.
 //   phase 1: {1 | last << 8, first segment, n segments, src0, P bytes, bases offset, 0, 0}
@@ -1032,12 +1052,13 @@ struct StageDesc {
     uint4 a, b;
 };
 
-// A16: per-destination counters are 16-bit halves of 32-bit words (slot i in
-// word i >> 1), chosen by the host when no destination can receive >= 2^16
-// (halves the counter footprint, so the ring gets a deeper pipeline).
+// CB: bits per destination counter (32, 16 or 8; 16/8-bit counters are
+// packed 2/4 per 32-bit word), the narrowest the host can prove no
+// destination overflows in one step; smaller counters leave shared memory
+// for larger tiles and a deeper ring.
 // LEAN: no trace recording and no traffic counters (compiled out; the host
 // launches this instance only for runs with record == 0 and stats off).
-template <int PM, int RW, bool A16, bool LEAN>
+template <int PM, int RW, int CB, bool LEAN>
 __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys s, DevState st) {
     constexpr bool WIDE = RW == RW_WIDE;
     constexpr bool TINY = RW == RW_TINY;
@@ -1222,7 +1243,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
         for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
             const long long d0 = tile * T;
             const int nd = (int)min((long long)T, q - d0);
-            for (int i = threadIdx.x; i < acc_words<A16>(T); i += kTileThreads) acc[i] = 0;
+            for (int i = threadIdx.x; i < acc_words<CB>(T); i += kTileThreads) acc[i] = 0;
             consumer_sync(kTileThreads);
 
             // ---- phase 1: receive sums
@@ -1288,7 +1309,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     }
                     const uint32_t acc_s = smem_u32(acc);
 #pragma unroll
-                    for (int e = 0; e < kEpl; ++e) tile_acc_add<A16>(acc_s, w[e], v[e]);
+                    for (int e = 0; e < kEpl; ++e) tile_acc_add<CB>(acc_s, w[e], v[e]);
                     if (stats_on) {
 #pragma unroll
                         for (int e = 0; e < kEpl; ++e) stat[ST_EDGES] += ((w[e] >> kSrcBits) != (uint32_t)T);
@@ -1358,7 +1379,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     if (active) {
                         long long C = Cprev;
                         if (ds_open(dsv)) {
-                            const uint32_t gsum = A16 ? (acc[i >> 1] >> ((i & 1) << 4)) & 0xffffu : acc[i];
+                            const uint32_t gsum = tile_acc_get<CB>(acc, i);
                             C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
                         }
                         const int D = ds_next(dsv);
@@ -1386,7 +1407,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     }
                     long long C = Cprev;
                     if (open_prev) {
-                        const uint32_t gsum = A16 ? (acc[i >> 1] >> ((i & 1) << 4)) & 0xffffu : acc[i];
+                        const uint32_t gsum = tile_acc_get<CB>(acc, i);
                         C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
                     }
                     pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3,

@@ -92,7 +92,7 @@ struct snp_engine {
     int p_mode = P_BIT;
     long long p_common = 1;
     long long p_max = 0;      // largest produced amount
-    bool acc16 = false;       // tiled: 16-bit destination counters (acc_words)
+    int cbits = 32;           // tiled: destination counter bits (32, 16, 8; acc_words)
     long long in_edges = 0;
     int kind = RECV_PULL;
     bool tiled = false;
@@ -237,13 +237,13 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         const long long unit = e->p_mode == P_BIT ? 1 : std::max<long long>(1, e->p_max);
         long long worst = 0;
         for (uint32_t x : indeg) worst = std::max<long long>(worst, (long long)x * unit);
-        e->acc16 = worst < 65536;
-        if (const char* env = getenv("SNPB200_ACC16")) e->acc16 = e->acc16 && atoi(env) != 0;
+        e->cbits = worst < 256 ? 8 : (worst < 65536 ? 16 : 32);
+        if (const char* env = getenv("SNPB200_COUNTER_BITS")) e->cbits = std::max(e->cbits, atoi(env));
     }
     // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
     // (2 tiles per SM with 16-bit counters still leaves a 3 x 48 KB ring;
     // 4 per SM with 32-bit counters; measured on K3, profiles/r1_history.md)
-    long long per_sm = (e->acc16 && heavy.empty()) ? 2 : 4;  // heavy-rule systems: more, smaller tiles
+    long long per_sm = (e->cbits <= 16 && heavy.empty()) ? 2 : 4;  // heavy-rule systems: more, smaller tiles
     if (const char* env = getenv("SNPB200_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
     long long T = ceil_div(std::max<long long>(q, 1), per_sm * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
@@ -254,9 +254,11 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
     cudaFuncAttributes fa{};
-    CU(cudaFuncGetAttributes(&fa, tiled_step_kernel<P_BIT, RW_WIDE, false, false>));
+    CU(cudaFuncGetAttributes(&fa, tiled_step_kernel<P_BIT, RW_WIDE, 32, false>));
     const long long budget = (long long)smem_optin - (long long)fa.sharedSizeBytes - 128;
-    auto acc_b = [&](long long t) { return 4ll * (e->acc16 ? acc_words<true>((int)t) : acc_words<false>((int)t)); };
+    auto acc_b = [&](long long t) {
+        return 4ll * (e->cbits == 8 ? acc_words<8>((int)t) : (e->cbits == 16 ? acc_words<16>((int)t) : acc_words<32>((int)t)));
+    };
     T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
     // large systems: cap T so that the ring keeps 3 stages
     while (T > 32 * 64 && (budget - acc_b(T)) / (long long)kStageBytes < 3 &&
@@ -531,8 +533,19 @@ int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_
 // transpose are built on the device.
 template <int PM, int RW>
 void pick_tiled_rw(snp_engine* e) {
-    e->step_fn = e->acc16 ? tiled_step_kernel<PM, RW, true, false> : tiled_step_kernel<PM, RW, false, false>;
-    e->lean_fn = e->acc16 ? tiled_step_kernel<PM, RW, true, true> : tiled_step_kernel<PM, RW, false, true>;
+    switch (e->cbits) {
+        case 8:
+            e->step_fn = tiled_step_kernel<PM, RW, 8, false>;
+            e->lean_fn = tiled_step_kernel<PM, RW, 8, true>;
+            break;
+        case 16:
+            e->step_fn = tiled_step_kernel<PM, RW, 16, false>;
+            e->lean_fn = tiled_step_kernel<PM, RW, 16, true>;
+            break;
+        default:
+            e->step_fn = tiled_step_kernel<PM, RW, 32, false>;
+            e->lean_fn = tiled_step_kernel<PM, RW, 32, true>;
+    }
 }
 
 template <int PM>
@@ -995,7 +1008,9 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     if (e->tiled) {
         e->step_block = kTileThreads + 32;  // consumer warps + one TMA producer warp
         e->step_smem = (size_t)s.ring * kStageBytes +
-                       (size_t)(e->acc16 ? acc_words<true>(s.tile) : acc_words<false>(s.tile)) * sizeof(uint32_t);
+                       (size_t)(e->cbits == 8 ? acc_words<8>(s.tile)
+                                                 : (e->cbits == 16 ? acc_words<16>(s.tile) : acc_words<32>(s.tile))) *
+                           sizeof(uint32_t);
         CU(cudaFuncSetAttribute(e->step_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
         CU(cudaFuncSetAttribute(e->lean_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, e->step_block, e->step_smem));
@@ -1229,7 +1244,7 @@ int snp_engine_get_info(const snp_engine* e, snp_engine_info* info) {
     info->tile = e->sys.tile;
     info->n_tiles = e->sys.n_tiles;
     info->ring_stages = e->tiled ? e->sys.ring : 0;
-    info->counter_bits = e->tiled ? (e->acc16 ? 16 : 32) : 0;
+    info->counter_bits = e->tiled ? e->cbits : 0;
     info->stage_bytes = e->tiled ? (int64_t)kStageBytes : 0;
     return SNP_OK;
 }
