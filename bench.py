@@ -1,7 +1,7 @@
 """Benchmark: SNP steps/s at 10^7 neurons on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload k3|k4|k2] [--format compressed|ell|sparse]
+                    [--workload k3|k4|k2|k5] [--format compressed|ell|sparse]
                     [--variant pull|push] [--policy first|seeded] [--extra]
 
 Workload (default, BASELINE.json configs[2], "K3" of SURVEY.md 8): synth-v1,
@@ -24,9 +24,11 @@ per-step working set (~1.2 GB) is ~10x the 126 MB L2, so no flush is needed.
   as its thread-pool workers (engine.py:170-189), timed on a bounded sample.
 
 Multi-GPU (torchrun, N>1): weak scaling -- each rank owns a 10^7-neuron row
-shard of an (N x 10^7)-neuron system and the per-step production bits are
-exchanged with an NCCL all-gather (paper_2408_04343_b200/sharded.py); value
-is whole-job 10^7-neuron-steps/s.
+shard of an (N x 10^7)-neuron system; the per-step production bits are
+exchanged by the step kernels' NVLink peer stores (or, without peer access or
+with SNPB200_EXCHANGE=nccl, an NCCL all-gather); paper_2408_04343_b200/
+sharded.py.  value is whole-job 10^7-neuron-steps/s.  --workload k5 runs
+K5's 10^8-neuron system on one GPU.
 """
 
 from __future__ import annotations
@@ -54,7 +56,7 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["k3", "k4", "k2"], default="k3")
+    p.add_argument("--workload", choices=["k3", "k4", "k2", "k5"], default="k3")
     p.add_argument("--q", type=int, default=Q_K3)
     p.add_argument("--format", choices=["compressed", "ell", "sparse"], default="compressed")
     p.add_argument("--variant", choices=["tiled", "pull", "push"], default="tiled")
@@ -76,6 +78,8 @@ def make_workload(args, q=None):
     q = q or args.q
     if args.workload == "k2":
         return snp.sort_arrays(snp.SortInstance(4096)), "sort n=4096 (K2)"
+    if args.workload == "k5":
+        q = 10 * Q_K3  # K5's 10^8-neuron system on one GPU
     a = snp.synth_v1(q, with_delays=(args.workload == "k4"))
     return a, f"synth-v1 q={q} out-degree 16, 4 rules/neuron{', delays 0-3' if args.workload == 'k4' else ''}"
 
@@ -273,6 +277,8 @@ def main():
     unit = "steps/s"
     if args.workload == "k2":
         metric, unit = "SNP steps/sec, sort n=4096", "steps/s"
+    if args.workload == "k5":
+        metric, unit = "SNP steps/sec at 10^8 neurons (one GPU)", "steps/s"
     config = {"workload": "", "format": args.format, "variant": args.variant, "policy": args.policy,
               "l2": "working set >> 126 MB L2 (no flush needed)", "parallelism": f"rows/{args.gpus}"}
 
@@ -348,7 +354,8 @@ def extra_measurements(args) -> dict:
     cases = [("k3", "compressed", "pull", "first"), ("k3", "compressed", "push", "first"),
              ("k3", "ell", "push", "first"), ("k3", "compressed", "tiled", "seeded"),
              ("k4", "compressed", "tiled", "first"), ("k4", "compressed", "tiled", "seeded"),
-             ("k2", "compressed", "tiled", "first"), ("k2", "compressed", "pull", "first")]
+             ("k2", "compressed", "tiled", "first"), ("k2", "compressed", "pull", "first"),
+             ("k5", "compressed", "tiled", "first")]
     for wl, fmt, var, pol in cases:
         a2 = argparse.Namespace(**vars(args))
         a2.workload, a2.format, a2.variant, a2.policy = wl, fmt, var, pol
@@ -368,8 +375,9 @@ def extra_measurements(args) -> dict:
         alg = algorithmic_bytes(fmt, arrays.neuron_count, arrays.rule_count, res.stats_dict(), 30)
         ms = tot / args.steps
         out[f"{wl}/{fmt}/{var}/{pol}"] = {"steps_per_s": 1000.0 / ms, "ms_per_step": ms, "step_kernel_ms": kms,
-                                          "alg_bytes_per_step": alg, "alg_GBps_per_step": alg / (ms / 1000) / 1e9}
-        del prep, eng
+                                          "alg_bytes_per_step": alg, "alg_GBps_per_step": alg / (ms / 1000) / 1e9,
+                                          "neurons": arrays.neuron_count}
+        del prep, eng, arrays
     return out
 
 
