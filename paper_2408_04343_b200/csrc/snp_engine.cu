@@ -317,7 +317,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     const long long S = (long long)start[n_tiles];
     std::vector<unsigned long long> cur(start.begin(), start.end() - 1);
     std::vector<uint32_t> bsrc(S);
-    std::vector<uint16_t> bslot(S);
+    std::vector<uint32_t> bslot(S);
     for (long long i = 0; i < n_src; ++i) {
         const uint32_t xs = sh ? sh->xpos((uint32_t)i) : (uint32_t)i;
         for (uint32_t e2 = soff[i]; e2 < soff[i + 1]; ++e2) {
@@ -325,7 +325,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
             if (dst < lo || dst >= hi) continue;
             const unsigned long long pos = cur[(dst - lo) / T]++;
             bsrc[pos] = xs;
-            bslot[pos] = (uint16_t)((dst - lo) % T);
+            bslot[pos] = (uint32_t)((dst - lo) % T);
         }
     }
     // segments

@@ -3,7 +3,7 @@
 // reference build in snp_engine.cu (build_tiles), from the out-adjacency
 // already on the device:
 //
-//   1. edge keys:   key = destination tile, value = src << 16 | slot
+//   1. edge keys:   key = destination tile, value = src << 20 | slot
 //   2. stable radix sort by tile (CUB) -> each tile's in-edges in source order
 //   3. segmentation (warp per tile, greedy exactly as the host): segment
 //      start / count / base (src & ~31) / last source; then the 256-word
@@ -25,7 +25,7 @@ __global__ void ingest_keys_kernel(long long q, const uint32_t* __restrict__ sof
         for (uint32_t e = soff[i]; e < soff[i + 1]; ++e) {
             const uint32_t d = sdst[e];
             key[e] = d / T;
-            val[e] = ((unsigned long long)i << 16) | (d % T);
+            val[e] = ((unsigned long long)i << 20) | (d % T);
         }
     }
 }
@@ -59,7 +59,7 @@ __global__ void ingest_segments_kernel(long long n_tiles, const unsigned long lo
         uint32_t b = 0, n = kSegEdges, prev = 0;
         for (unsigned long long c = e0; c < e1; c += 32) {
             const unsigned long long my = c + lane;
-            const uint32_t v = my < e1 ? (uint32_t)(val[my] >> 16) : 0u;
+            const uint32_t v = my < e1 ? (uint32_t)(val[my] >> 20) : 0u;
             const int cnt = (int)min(32ull, e1 - c);
             for (int k = 0; k < cnt; ++k) {
                 const uint32_t src = __shfl_sync(0xffffffffu, v, k);
@@ -95,7 +95,7 @@ __global__ void ingest_segments_kernel(long long n_tiles, const unsigned long lo
     }
 }
 
-// 3b. warp per segment: the 256 words (slot << 17 | src - base, padding T << 17)
+// 3b. warp per segment: the 256 words (slot << kSrcBits | src - base, padding T << kSrcBits)
 __global__ void ingest_words_kernel(long long nseg, const unsigned long long* __restrict__ seg_first,
                                     const uint32_t* __restrict__ seg_n, const uint32_t* __restrict__ seg_base,
                                     const unsigned long long* __restrict__ val, uint32_t T, uint32_t* __restrict__ words) {
@@ -108,7 +108,7 @@ __global__ void ingest_words_kernel(long long nseg, const unsigned long long* __
             uint32_t w = T << kSrcBits;
             if ((uint32_t)p < n) {
                 const unsigned long long v = val[f + p];
-                w = ((uint32_t)(v & 0xffffu) << kSrcBits) | ((uint32_t)(v >> 16) - b);
+                w = ((uint32_t)(v & 0xfffffu) << kSrcBits) | ((uint32_t)(v >> 20) - b);
             }
             words[g * kSegEdges + p] = w;
         }

@@ -300,3 +300,30 @@ def test_peer_exchange_two_processes_ipc():
     np.testing.assert_array_equal(np.concatenate([got[0][0], got[1][0]]), want.config)
     np.testing.assert_array_equal(np.concatenate([got[0][1], got[1][1]]), want.delays)
     assert got[0][2] == got[1][2] == want.steps
+
+
+@pytest.mark.gpu
+def test_k5_scale_sharded_equals_single_and_oracle():
+    """K5-sized system (10^8 neurons, 1.6 x 10^9 synapses): 2-rank peer-exchange
+    partition == single engine after 3 steps, and the single engine == the C
+    oracle after 2 steps (SURVEY.md 8(e) parity at K5 scale, one GPU)."""
+    import psutil
+    if psutil.virtual_memory().total < 120 * 2**30 or torch.cuda.get_device_properties(0).total_memory < 100 * 2**30:
+        pytest.skip("needs >= 120 GB host RAM and a B200-class device")
+    from oracle import coracle
+    from oracle.snp_oracle import OracleSystem
+    q = 100_000_000
+    a = snp.synth_v1(q, with_delays=True)
+    sel = snp.SeededRandom(11)
+    single = snp.prepare(a, snp.Format.COMPRESSED)
+    want3 = snp.run_final(single, snp.SimOptions(max_steps=3, selection=sel))
+    want2 = snp.run_final(single, snp.SimOptions(max_steps=2, selection=sel))
+    del single
+    _, oc, od = coracle.run(OracleSystem.from_arrays(a), 2, 1, 11)
+    np.testing.assert_array_equal(want2.config, oc)
+    np.testing.assert_array_equal(want2.delays, od)
+    del oc, od
+    cfg, dly, steps, halt = _run_p2p_on_one_gpu(a, 2, 3, sel)
+    np.testing.assert_array_equal(cfg, want3.config)
+    np.testing.assert_array_equal(dly, want3.delays)
+    assert steps == 3
