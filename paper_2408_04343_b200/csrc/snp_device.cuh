@@ -54,7 +54,7 @@ constexpr int kTileThreads = SNP_TILE_THREADS;  // consumer threads per CTA (mul
 static_assert(kTileThreads % 32 == 0 && kTileThreads + 32 <= 1024, "CTA must fit 1024 threads");
 constexpr int kSegEdges = 256;            // one warp pass: 8 consecutive words per lane
 #ifndef SNP_SRC_BITS
-#define SNP_SRC_BITS 16
+#define SNP_SRC_BITS 15
 #endif
 constexpr uint32_t kSrcBits = SNP_SRC_BITS;  // source offset within a segment
 constexpr uint32_t kDstBits = 32 - kSrcBits; // destination slot within a tile

@@ -244,6 +244,10 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     // (2 tiles per SM with 16-bit counters still leaves a 3 x 48 KB ring;
     // 4 per SM with 32-bit counters; measured on K3, profiles/r1_history.md)
     long long per_sm = (e->cbits <= 16 && heavy.empty()) ? 2 : 4;  // heavy-rule systems: more, smaller tiles
+    // sources spread over >= 4x this engine's rows (row partition at 4+ ranks):
+    // each tile's P windows span all sources, so fewer, larger tiles read
+    // fewer window bytes per edge (large systems)
+    if (per_sm == 2 && n_src >= 4 * std::max<long long>(q, 1)) per_sm = 1;
     if (const char* env = getenv("SNPB200_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
     long long T = ceil_div(std::max<long long>(q, 1), per_sm * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
