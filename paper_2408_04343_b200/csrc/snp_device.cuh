@@ -144,6 +144,18 @@ struct DevSys {
     long long x_stride;         // words per rank chunk (0 = not sharded)
     int world;
     int rank;
+    // two-pass receive (variant TILED2, large source ranges): pass 1 turns
+    // each source window's P bits into one bit per in-edge (tp_bits, grouped
+    // 32 per word in tile order); the tiled kernel's phase 1 then streams
+    // 16-bit destination slots + those bits instead of segments + P windows
+    int tp;                       // 1 = two-pass layout
+    int tp_wlog;                  // log2 source-window size
+    long long tp_nw;              // source windows
+    const uint16_t* tp_slots;     // [groups * 32] destination slots, tile order (padding = T)
+    uint32_t* tp_bits;            // [groups] per-step edge bits, tile order
+    const uint16_t* tp_off;       // [groups * 32] source offsets in the window, window order
+    const uint32_t* tp_gword;     // [groups] window-order group -> tile-order group
+    const uint32_t* tp_wgroup;    // [tp_nw + 1] window -> first window-order group
     // peer exchange (NVLink P2P): every rank's exchange block (3 slots of
     // p_words words, then `world` 64-bit step flags), mapped into this process
     const unsigned long long* peers;
@@ -1032,6 +1044,20 @@ __device__ __forceinline__ void tile_acc_add(uint32_t acc_s, uint32_t w, uint32_
     }
 }
 
+// Two-pass phase 1: add v to the counter of a plain slot index.
+template <int CB>
+__device__ __forceinline__ void tile_acc_add_slot(uint32_t acc_s, uint32_t slot, uint32_t v) {
+    if (CB == 16) {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(acc_s + ((slot >> 1) << 2)), "r"(v << ((slot & 1u) << 4))
+                     : "memory");
+    } else if (CB == 8) {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(acc_s + ((slot >> 2) << 2)), "r"(v << ((slot & 3u) << 3))
+                     : "memory");
+    } else {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(acc_s + (slot << 2)), "r"(v) : "memory");
+    }
+}
+
 // Counter of destination i (phase 2).
 template <int CB>
 __device__ __forceinline__ uint32_t tile_acc_get(const uint32_t* acc, int i) {
@@ -1205,7 +1231,18 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                         h->last = kind >> 8;
                         h->first = first;
                         h->n = n;
-                        if ((kind & 0xff) == 1) {
+                        if ((kind & 0xff) == 3) {
+                            // two-pass phase 1: first = group, n groups; slots + edge bits
+                            const uint32_t sbytes = n * 64u, ga = first & ~3u, bbytes = round16((n + (first & 3u)) * 4u);
+                            h->src0 = first & 3u;
+                            if (n) {
+                                mbar_expect_tx(&full_bar[b], sbytes + bbytes);
+                                bulk_g2s(buf + kPayload, s.tp_slots + (size_t)first * 32, sbytes, &full_bar[b]);
+                                bulk_g2s(buf + kPayload + sbytes, s.tp_bits + ga, bbytes, &full_bar[b]);
+                            } else {
+                                mbar_expect_tx(&full_bar[b], 0);  // empty stage: the arrival alone completes it
+                            }
+                        } else if ((kind & 0xff) == 1) {
                             // f3 = src0, f4 = P bytes, f5 = bases offset
                             const uint32_t wbytes = n * kSegEdges * 4u, bbytes = round16(n * 4u);
                             h->src0 = f3;
@@ -1257,6 +1294,37 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 }
                 const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
                 const uint32_t n = h->n, last = h->last, src0 = h->src0;
+                if (h->kind == 3) {
+                    // two-pass: 32 edges per group = 32 slots + one word of edge bits
+                    const uint16_t* sl = reinterpret_cast<const uint16_t*>(buf + kPayload);
+                    const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf + kPayload + n * 64u) + src0;
+                    const uint32_t acc_s = smem_u32(acc);
+                    const uint32_t groups = (s.dbg & 1) ? 0u : n;
+                    uint32_t i = warp;
+                    for (; i + 3u * kWarpsC < groups; i += 4u * kWarpsC) {
+                        uint32_t sv[4], bv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            sv[u] = sl[(i + u * kWarpsC) * 32u + lane];
+                            bv[u] = (bw[i + u * kWarpsC] >> lane) & 1u;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) tile_acc_add_slot<CB>(acc_s, sv[u], bv[u]);
+                        if (stats_on) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) stat[ST_EDGES] += sv[u] != (uint32_t)T;
+                        }
+                    }
+                    for (; i < groups; i += kWarpsC) {
+                        const uint32_t sv = sl[i * 32u + lane];
+                        tile_acc_add_slot<CB>(acc_s, sv, (bw[i] >> lane) & 1u);
+                        if (stats_on) stat[ST_EDGES] += sv != (uint32_t)T;
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[b]);
+                    if (last) break;
+                    continue;
+                }
                 const bool pst = h->pstaged != 0;
                 const uint32_t* ps = reinterpret_cast<const uint32_t*>(buf + kPayload + n * kSegEdges * 4u);
                 // work unit: 1/kSegSplit of a segment (kEpl edges per lane), so the
@@ -1537,6 +1605,56 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
         finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0,
                     s.x_stride ? Pcur + (long long)s.rank * s.x_stride + s.x_stride - 4 : nullptr,
                     s.p2p ? &s : nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Two-pass receive, pass 1 (variant TILED2): one CTA per source window.  The
+// window's P_{k-1} bits (<= 2^17 sources, 16 KB) are read once into shared
+// memory; each group of 32 in-edges (window order) becomes one word of edge
+// bits, stored at its tile-order position for the tiled kernel's phase 1.
+constexpr int kMaxWindowWords = (1 << 17) / 32;
+
+__global__ void __launch_bounds__(256) pass1_kernel(DevSys s, DevState st) {
+    __shared__ uint32_t pw[kMaxWindowWords];
+    __shared__ int x_ok;
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    const long long k = vc->step;
+    if (vc->halted || k >= vc->stop_at) return;
+    if (s.p2p && k > 0) {
+        if (threadIdx.x == 0) x_ok = wait_peers(s, vc->epoch, k - 1) ? 1 : 0;
+        __syncthreads();
+        if (!x_ok) return;  // the step kernel reports the timeout
+    }
+    const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t wwords = 1u << (s.tp_wlog - 5);
+    for (long long w = blockIdx.x; w < s.tp_nw; w += gridDim.x) {
+        const uint32_t* src = Pprev + w * wwords;
+        for (uint32_t i = threadIdx.x; i < wwords; i += blockDim.x) pw[i] = __ldcg(src + i);
+        __syncthreads();
+        const uint32_t g0 = __ldg(s.tp_wgroup + w), g1 = __ldg(s.tp_wgroup + w + 1);
+        uint32_t g = g0 + warp;
+        for (; g + 3u * nwarps < g1; g += 4u * nwarps) {
+            uint32_t o[4], d[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                o[u] = __ldg(s.tp_off + (size_t)(g + u * nwarps) * 32 + lane);
+                d[u] = __ldg(s.tp_gword + g + u * nwarps);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned bits = __ballot_sync(0xffffffffu, (pw[o[u] >> 5] >> (o[u] & 31u)) & 1u);
+                if (lane == 0) s.tp_bits[d[u]] = bits;
+            }
+        }
+        for (; g < g1; g += nwarps) {
+            const uint32_t o = __ldg(s.tp_off + (size_t)g * 32 + lane);
+            const unsigned bits = __ballot_sync(0xffffffffu, (pw[o >> 5] >> (o & 31u)) & 1u);
+            if (lane == 0) s.tp_bits[__ldg(s.tp_gword + g)] = bits;
+        }
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -134,6 +134,8 @@ struct snp_engine {
     unsigned long long* d_digest = nullptr;  // SNP_REC_DIGEST row digests (3 x digest_cap)
     long long digest_cap = 0;
     long long n_stages = 0, n_sbases = 0;   // tiled layout sizes (layout digest)
+    int p1_grid = 0;                        // two-pass: pass-1 CTAs
+    long long p_bit_words = 0;              // P_BIT: words per P buffer (single engine)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
 
@@ -199,6 +201,32 @@ struct ShardInput {
 // CSR out-adjacency is source-major, so a stable bucket pass keeps that
 // order), are packed into 256-edge segments whose sources span < 2^17.
 int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, long long S, bool stage_p);
+int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, const std::vector<uint32_t>& soff,
+                 const std::vector<uint32_t>& sdst, const ShardInput* sh, const std::vector<uint32_t>& roff_h);
+
+// Phase-2 stage descriptors of tile t (kSub destinations each, with their
+// rule words when they fit a stage).
+void append_phase2_desc(const snp_engine* e, long long t, const std::vector<uint32_t>& roff_h,
+                        std::vector<StageDesc>& desc) {
+    const DevSys& s = e->sys;
+    const long long T = s.tile, q = e->q;
+    const uint32_t rw_size = e->tiny_rules ? 4u : (e->wide_rules ? 16u : 8u);
+    auto r16 = [](unsigned long long x) { return (uint32_t)((x + 15) & ~15ull); };
+    const long long d0 = t * T;
+    const long long nd = std::min<long long>(T, q - d0);
+    for (long long dd = 0; dd < nd; dd += kSub) {
+        const uint32_t n = (uint32_t)std::min<long long>(kSub, nd - dd);
+        const uint32_t rf = roff_h[d0 + dd], rl = roff_h[d0 + dd + n];
+        const uint32_t r_al = e->tiny_rules ? (rf & ~3u) : (e->wide_rules ? rf : (rf & ~1u));
+        const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + (s.rpn ? 0u : r16((n + 1) * 4ull));
+        uint32_t rb = r16((unsigned long long)(rl - r_al) * rw_size);
+        if (fixed + rb > kStageBytes) rb = 0;
+        StageDesc sd;
+        sd.a = make_uint4(2u | ((dd + kSub >= nd) ? 256u : 0u), (uint32_t)dd, n, r_al);
+        sd.b = make_uint4(rb, 0, 0, 0);
+        desc.push_back(sd);
+    }
+}
 
 int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff_in,
                 const std::vector<uint32_t>& sdst_in, const std::vector<uint32_t>& roff_h,
@@ -263,7 +291,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     auto acc_b = [&](long long t) {
         return 4ll * (e->cbits == 8 ? acc_words<8>((int)t) : (e->cbits == 16 ? acc_words<16>((int)t) : acc_words<32>((int)t)));
     };
-    T = std::min<long long>(kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
+    T = std::min<long long>(s.tp ? 65504 : kMaxTile, std::max<long long>(32, (T + 31) / 32 * 32));
     // large systems: cap T so that the ring keeps 3 stages
     while (T > 32 * 64 && (budget - acc_b(T)) / (long long)kStageBytes < 3 &&
            (budget - acc_b(T - 32)) / (long long)kStageBytes >= 1)
@@ -310,6 +338,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     }
     // the layout itself: on the device (default for a single engine with its
     // out-adjacency on the device), or the host reference build below
+    if (s.tp) return build_tiles2(e, d_soff, d_sdst, soff, sdst, sh, roff_h);
     bool dev_build = !sh && d_soff && d_sdst && sdst.size() < (1ull << 31);
     if (const char* env = getenv("SNPB200_DEVICE_BUILD")) dev_build = dev_build && atoi(env) != 0;
     if (dev_build) return build_tiles_device(e, d_soff, d_sdst, (long long)sdst.size(), stage_p);
@@ -387,20 +416,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
             desc.push_back(sd);
             g += n;
         } while (g < g1);
-        const long long d0 = t * T;
-        const long long nd = std::min<long long>(T, q - d0);
-        for (long long dd = 0; dd < nd; dd += kSub) {
-            const uint32_t n = (uint32_t)std::min<long long>(kSub, nd - dd);
-            const uint32_t rf = roff_h[d0 + dd], rl = roff_h[d0 + dd + n];
-            const uint32_t r_al = e->tiny_rules ? (rf & ~3u) : (e->wide_rules ? rf : (rf & ~1u));
-            const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + (s.rpn ? 0u : r16((n + 1) * 4ull));
-            uint32_t rb = r16((unsigned long long)(rl - r_al) * rw_size);
-            if (fixed + rb > kStageBytes) rb = 0;
-            StageDesc sd;
-            sd.a = make_uint4(2u | ((dd + kSub >= nd) ? 256u : 0u), (uint32_t)dd, n, r_al);
-            sd.b = make_uint4(rb, 0, 0, 0);
-            desc.push_back(sd);
-        }
+        append_phase2_desc(e, t, roff_h, desc);
         tstage[t + 1] = (uint32_t)desc.size();
     }
     StageDesc* d_desc;
@@ -529,6 +545,159 @@ int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_
     e->in_edges = nseg * kSegEdges;
     e->n_stages = tstage[n_tiles];
     e->n_sbases = (long long)tsbase[n_tiles] + 4;
+    return SNP_OK;
+}
+
+// Two-pass layout (variant TILED2, snp_ingest.cuh): edges sorted by (tile,
+// source window) on the device; per 32-edge group a tile-order slot block
+// and a window-order offset block; host-side scans of the small per-chunk
+// counts; phase-1 stage descriptors are runs of groups.
+int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, const std::vector<uint32_t>& soff,
+                 const std::vector<uint32_t>& sdst, const ShardInput* sh, const std::vector<uint32_t>& roff_h) {
+    DevSys& s = e->sys;
+    const long long q = e->q, nt = s.n_tiles, T = s.tile;
+    if (T > 65535 - 1) return fail(SNP_ERR_CAPACITY, "two-pass tiles need T < 65535");
+    const long long space = sh ? (long long)sh->world * (sh->nl + 128) : std::max<long long>(q, 1);
+    int wlog = 12;
+    while (wlog < 16 && (1ll << wlog) < 32 * space / std::max<long long>(T, 1)) ++wlog;
+    if (const char* env = getenv("SNPB200_WINDOW_LOG")) wlog = std::min(16, std::max(5, atoi(env)));
+    const long long nw = ceil_div(space, 1ll << wlog);
+    const long long nk = nt * nw;
+    if (nk >= (1ll << 32) - 1) return fail(SNP_ERR_CAPACITY, "two-pass layout: tiles x windows exceeds 2^32");
+    TmpAllocs tmp;
+    // edges -> keys / values on the device
+    long long S;
+    uint32_t *k_in, *k_out;
+    unsigned long long *v_in, *v_out;
+    if (!sh) {
+        S = (long long)sdst.size();
+        CU(tmp.get(&k_in, S));
+        CU(tmp.get(&v_in, S));
+        if (q > 0 && S > 0)
+            tp_keys_csr_kernel<<<grid_for(q), 256>>>(q, d_soff, d_sdst, (uint32_t)T, (uint32_t)wlog, (uint32_t)nw, k_in, v_in);
+    } else {
+        std::vector<uint32_t> xs, ld;
+        for (long long i = 0; i < sh->q_global; ++i) {
+            const uint32_t x = sh->xpos((uint32_t)i);
+            for (uint32_t e2 = soff[i]; e2 < soff[i + 1]; ++e2) {
+                const long long dst = sdst[e2];
+                if (dst < sh->lo || dst >= sh->hi) continue;
+                xs.push_back(x);
+                ld.push_back((uint32_t)(dst - sh->lo));
+            }
+        }
+        S = (long long)xs.size();
+        uint32_t *d_xs, *d_ld;
+        CU(tmp.get(&d_xs, S));
+        CU(tmp.get(&d_ld, S));
+        CU(cudaMemcpy(d_xs, xs.data(), S * 4, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(d_ld, ld.data(), S * 4, cudaMemcpyHostToDevice));
+        CU(tmp.get(&k_in, S));
+        CU(tmp.get(&v_in, S));
+        if (S > 0)
+            tp_keys_list_kernel<<<grid_for(S), 256>>>(S, d_xs, d_ld, (uint32_t)T, (uint32_t)wlog, (uint32_t)nw, k_in, v_in);
+    }
+    CU(cudaGetLastError());
+    if (S >= (1ll << 31)) return fail(SNP_ERR_CAPACITY, "two-pass layout: more than 2^31 in-edges");
+    CU(tmp.get(&k_out, S));
+    CU(tmp.get(&v_out, S));
+    int bits = 1;
+    while ((1ll << bits) <= nk) ++bits;
+    size_t temp_bytes = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, k_in, k_out, v_in, v_out, (int)S, 0, bits));
+    unsigned char* temp;
+    CU(tmp.get(&temp, (long long)temp_bytes));
+    if (S > 0) CU(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, (int)S, 0, bits));
+    // per-chunk counts and the three offset tables (host scans)
+    uint32_t* d_cnt;
+    CU(tmp.get(&d_cnt, nk));
+    CU(cudaMemset(d_cnt, 0, nk * 4));
+    if (S > 0) tp_hist_kernel<<<grid_for(S), 256>>>(S, k_out, d_cnt);
+    CU(cudaGetLastError());
+    std::vector<uint32_t> cnt(nk);
+    CU(cudaMemcpy(cnt.data(), d_cnt, nk * 4, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> off_raw(nk + 1, 0), off2(nk + 1, 0), off1(nk + 1, 0);
+    for (long long k = 0; k < nk; ++k) {
+        off_raw[k + 1] = off_raw[k] + cnt[k];
+        off2[k + 1] = off2[k] + ((cnt[k] + 31ull) & ~31ull);
+    }
+    {
+        unsigned long long acc = 0;
+        for (long long w = 0; w < nw; ++w)
+            for (long long t = 0; t < nt; ++t) {
+                off1[w * nt + t] = acc;
+                acc += (cnt[t * nw + w] + 31ull) & ~31ull;
+            }
+        off1[nk] = acc;
+    }
+    const long long edges = (long long)off2[nk], groups = edges / 32;
+    if (edges >= (1ll << 32)) return fail(SNP_ERR_CAPACITY, "two-pass layout exceeds 2^32 edge slots");
+    unsigned long long *d_raw, *d_off2, *d_off1;
+    CU(tmp.get(&d_raw, nk + 1));
+    CU(tmp.get(&d_off2, nk + 1));
+    CU(tmp.get(&d_off1, nk + 1));
+    CU(cudaMemcpy(d_raw, off_raw.data(), (nk + 1) * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_off2, off2.data(), (nk + 1) * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_off1, off1.data(), (nk + 1) * 8, cudaMemcpyHostToDevice));
+    uint16_t *d_slots, *d_offs;
+    uint32_t *d_gword, *d_bits;
+    TRY(e->alloc(&d_slots, edges + 64));
+    TRY(e->alloc(&d_offs, edges + 64));
+    TRY(e->alloc(&d_gword, groups + 4));
+    TRY(e->alloc(&d_bits, groups + 8));
+    CU(cudaMemset(d_bits, 0, (groups + 8) * 4));
+    CU(cudaMemset(d_offs, 0, (edges + 64) * 2));
+    fill_u16_kernel<<<grid_for(std::min<long long>(edges + 64, 148ll * 4096)), 256>>>(edges + 64, d_slots, (uint16_t)T);
+    CU(cudaGetLastError());
+    if (S > 0)
+        tp_fill_kernel<<<grid_for(S), 256>>>(S, k_out, v_out, d_raw, d_off2, d_off1, (uint32_t)nt, (uint32_t)nw,
+                                             (uint32_t)wlog, d_slots, d_offs);
+    tp_gword_kernel<<<grid_for(nk), 256>>>(nk, d_cnt, d_off2, d_off1, (uint32_t)nt, (uint32_t)nw, d_gword);
+    CU(cudaGetLastError());
+    // window -> first group (window order), tile -> group range (tile order)
+    std::vector<uint32_t> wgroup(nw + 1), tgroup(nt + 1);
+    for (long long w = 0; w <= nw; ++w) wgroup[w] = (uint32_t)(off1[std::min<long long>(w * nt, nk)] / 32);
+    for (long long t = 0; t <= nt; ++t) tgroup[t] = (uint32_t)(off2[std::min<long long>(t * nw, nk)] / 32);
+    uint32_t* d_wgroup;
+    TRY(upload(e, &d_wgroup, wgroup));
+    // stage descriptors: phase-1 runs of groups, then the phase-2 stages
+    const uint32_t G = (kStageBytes - kPayload - 32) / 68;
+    std::vector<StageDesc> desc;
+    std::vector<uint32_t> tstage(nt + 1, 0);
+    for (long long t = 0; t < nt; ++t) {
+        uint32_t g = tgroup[t];
+        const uint32_t g1 = tgroup[t + 1];
+        do {
+            const uint32_t n = std::min<uint32_t>(G, g1 - g);
+            StageDesc sd;
+            sd.a = make_uint4(3u | ((g + n >= g1) ? 256u : 0u), g, n, 0);
+            sd.b = make_uint4(0, 0, 0, 0);
+            desc.push_back(sd);
+            g += n;
+        } while (g < g1);
+        append_phase2_desc(e, t, roff_h, desc);
+        tstage[t + 1] = (uint32_t)desc.size();
+    }
+    StageDesc* d_desc;
+    uint32_t *d_tstage, *d_sb;
+    TRY(upload(e, &d_desc, desc));
+    TRY(upload(e, &d_tstage, tstage));
+    TRY(e->alloc(&d_sb, 4));
+    CU(cudaMemset(d_sb, 0, 16));
+    CU(cudaDeviceSynchronize());
+    s.stages = d_desc;
+    s.tstage = d_tstage;
+    s.stage_bases = d_sb;
+    s.tp_wlog = wlog;
+    s.tp_nw = nw;
+    s.tp_slots = d_slots;
+    s.tp_bits = d_bits;
+    s.tp_off = d_offs;
+    s.tp_gword = d_gword;
+    s.tp_wgroup = d_wgroup;
+    e->in_edges = edges;
+    e->n_stages = (long long)desc.size();
+    e->p1_grid = (int)std::max<long long>(1, std::min<long long>(nw, 148ll * 8));
     return SNP_OK;
 }
 
@@ -747,12 +916,14 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             e->variant = (!sh && 2 * heavy_rules > m) ? SNP_VARIANT_PULL : SNP_VARIANT_TILED;
         }
         e->kind = e->variant == SNP_VARIANT_PUSH ? RECV_ARRAY : RECV_PULL;
-        e->tiled = e->variant == SNP_VARIANT_TILED;
+        e->tiled = e->variant == SNP_VARIANT_TILED || e->variant == SNP_VARIANT_TILED2;
+        e->sys.tp = e->variant == SNP_VARIANT_TILED2 ? 1 : 0;
     } else {
         e->variant = SNP_VARIANT_PUSH;
         e->kind = RECV_ARRAY;
     }
     e->p_max = pmax;
+    if (e->sys.tp && !pcommon) e->sys.tp = 0;  // two-pass receive moves P bits only
     if (pcommon) {
         e->p_mode = P_BIT;
         e->p_common = pfirst > 0 ? pfirst : 1;
@@ -952,16 +1123,22 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         s.rank = sh->rank;
         s.gbase = sh->lo;
         s.xbase = (long long)sh->rank * s.x_stride * 32;
-        e->p_words = s.x_stride * sh->world + 8;
+        // identical on every rank (peers address each other's flags at
+        // 3 * p_words): the two-pass tail covers any window size <= 2^16
+        e->p_words = s.x_stride * sh->world + 8 + (s.tp ? (1ll << (16 - 5)) : 0);
     }
     if (e->kind == RECV_PULL) {
         long long words;
         switch (e->p_mode) {
-            case P_BIT: words = sh ? e->p_words : ceil_div(q + 1, 32) + 8; break;  // +8: bulk-copy tails
+            case P_BIT:  // +8: bulk-copy tails; two-pass: whole source windows
+                words = sh ? e->p_words
+                           : std::max<long long>(ceil_div(q + 1, 32) + 8, s.tp ? s.tp_nw * (1ll << (s.tp_wlog - 5)) + 8 : 0);
+                break;
             case P_U8: words = ceil_div(q + 1, 4) + 1; break;
             case P_U16: words = ceil_div(q + 1, 2) + 1; break;
             default: words = q + 2; break;
         }
+        if (e->p_mode == P_BIT && !sh) e->p_bit_words = words;
         if (sh) {
             // one exchange block: 3 slots, then `world` 64-bit step flags (peer
             // exchange); a single allocation so it maps with one IPC handle
@@ -1034,8 +1211,15 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
 }
 
 // Launch one step's kernels on the engine stream; returns launch count.
+// Two-pass receive: pass 1 (edge bits per source window) before the step kernel.
+int launch_pass1(snp_engine* e) {
+    if (!e->sys.tp) return 0;
+    pass1_kernel<<<e->p1_grid, 256, 0, e->stream>>>(e->sys, e->st);
+    return 1;
+}
+
 int launch_step(snp_engine* e, long long* row_visits = nullptr) {
-    int n = 1;
+    int n = 1 + launch_pass1(e);
     run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
     if (e->kind == RECV_ARRAY) {
         if (e->format == SNP_FMT_SPARSE) {
@@ -1074,7 +1258,7 @@ int reset_state(snp_engine* e) {
         for (int i = 0; i < 3; ++i) {
             size_t bytes;
             switch (e->p_mode) {
-                case P_BIT: bytes = (e->p_words ? e->p_words : ceil_div(q + 1, 32) + 8) * 4; break;
+                case P_BIT: bytes = (e->p_words ? e->p_words : e->p_bit_words) * 4; break;
                 case P_U8: bytes = (ceil_div(q + 1, 4) + 1) * 4; break;
                 case P_U16: bytes = (ceil_div(q + 1, 2) + 1) * 4; break;
                 default: bytes = (q + 2) * 4; break;
@@ -1131,7 +1315,7 @@ int ensure_graph(snp_engine* e, long long iters) {
 }
 
 int kernels_per_step(const snp_engine* e) {
-    if (e->kind == RECV_PULL) return 1;
+    if (e->kind == RECV_PULL) return e->sys.tp ? 2 : 1;
     return e->format == SNP_FMT_SPARSE ? 2 : 3;
 }
 
@@ -1214,7 +1398,7 @@ int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
         ld.adj_offsets = nullptr;
         ld.adj_targets = nullptr;
         ld.syn_target = nullptr;
-        ld.variant = SNP_VARIANT_TILED;
+        ld.variant = desc->variant == SNP_VARIANT_TILED2 ? SNP_VARIANT_TILED2 : SNP_VARIANT_TILED;
         e->shard_lo = sh.lo;
         e->shard_hi = sh.hi;
         e->shard_nl = sh.nl;
@@ -1430,6 +1614,7 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
         for (auto& x : ev) CU(cudaEventCreate(&x));
         CU(cudaEventRecord(e->ev0, e->stream));
         for (long long i = 0; i < steps; ++i) {
+            launches += launch_pass1(e);
             CU(cudaEventRecord(ev[2 * i], e->stream));
             run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
             CU(cudaEventRecord(ev[2 * i + 1], e->stream));
@@ -1524,6 +1709,7 @@ int snp_sv_calc(snp_engine* e, const int64_t* config, const int64_t* delays, int
     c.seed = seed;
     c.record = REC_SPIKING;
     TRY(push_ctrl(e));
+    launch_pass1(e);
     e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
     CU(cudaGetLastError());
     if (q > 0) {
@@ -1580,6 +1766,7 @@ int snp_step(snp_engine* e, const int64_t* config, const int64_t* delays, const 
         }
         CU(cudaGetLastError());
     }
+    launch_pass1(e);
     e->step_fn<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);  // finalize only
     CU(cudaGetLastError());
     TRY(pull_ctrl(e));
@@ -1684,6 +1871,27 @@ static int connect_peers(snp_engine* e, const std::vector<unsigned long long>& b
 }
 
 int snp_engine_layout_digest(const snp_engine* e, uint64_t* out) {
+    if (e && e->sys.tp) {
+        // two-pass layout: slots, offsets (as u32 pairs), gword, stages, tstage, window groups
+        if (!out) return fail(SNP_ERR_BAD_ARG, "null argument");
+        memset(out, 0, 6 * sizeof(uint64_t));
+        CU(cudaSetDevice(e->device));
+        const DevSys& s = e->sys;
+        unsigned long long* d;
+        CU(cudaMalloc(&d, 6 * 8));
+        CU(cudaMemset(d, 0, 6 * 8));
+        const long long groups = e->in_edges / 32;
+        const long long n[6] = {groups * 16, groups * 16, groups, e->n_stages * 8, s.n_tiles + 1, s.tp_nw + 1};
+        const uint32_t* a[6] = {reinterpret_cast<const uint32_t*>(s.tp_slots), reinterpret_cast<const uint32_t*>(s.tp_off),
+                                s.tp_gword, reinterpret_cast<const uint32_t*>(s.stages), s.tstage, s.tp_wgroup};
+        for (int i = 0; i < 6; ++i)
+            if (n[i] > 0) digest_u32_kernel<<<grid_for(std::min<long long>(n[i], 148ll * 1024)), 256>>>(n[i], a[i], d + i);
+        cudaError_t err = cudaGetLastError();
+        if (err == cudaSuccess) err = cudaMemcpy(out, d, 6 * 8, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        CU(err);
+        return SNP_OK;
+    }
     if (!e || !out) return fail(SNP_ERR_BAD_ARG, "null argument");
     memset(out, 0, 6 * sizeof(uint64_t));
     if (!e->tiled) return SNP_OK;

@@ -201,3 +201,69 @@ __global__ void digest_u32_kernel(long long n, const uint32_t* __restrict__ a, u
 }
 
 }  // namespace snp
+
+namespace snp {
+
+// ---- two-pass layout (variant TILED2) ----------------------------------------
+// key = tile * nw + window (tile order), value = xsrc << 20 | slot
+
+__global__ void tp_keys_csr_kernel(long long q, const uint32_t* __restrict__ soff, const uint32_t* __restrict__ sdst,
+                                   uint32_t T, uint32_t wlog, uint32_t nw, uint32_t* __restrict__ key,
+                                   unsigned long long* __restrict__ val) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (long long)gridDim.x * blockDim.x) {
+        for (uint32_t e = soff[i]; e < soff[i + 1]; ++e) {
+            const uint32_t d = sdst[e];
+            key[e] = (d / T) * nw + ((uint32_t)i >> wlog);
+            val[e] = ((unsigned long long)i << 20) | (d % T);
+        }
+    }
+}
+
+__global__ void tp_keys_list_kernel(long long S, const uint32_t* __restrict__ xsrc, const uint32_t* __restrict__ ldst,
+                                    uint32_t T, uint32_t wlog, uint32_t nw, uint32_t* __restrict__ key,
+                                    unsigned long long* __restrict__ val) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < S; e += (long long)gridDim.x * blockDim.x) {
+        const uint32_t d = ldst[e], x = xsrc[e];
+        key[e] = (d / T) * nw + (x >> wlog);
+        val[e] = ((unsigned long long)x << 20) | (d % T);
+    }
+}
+
+__global__ void tp_hist_kernel(long long S, const uint32_t* __restrict__ key, uint32_t* __restrict__ cnt) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < S; e += (long long)gridDim.x * blockDim.x)
+        atomicAdd(cnt + key[e], 1u);
+}
+
+// sorted edge i -> its tile-order slot and window-order source offset
+__global__ void tp_fill_kernel(long long S, const uint32_t* __restrict__ key, const unsigned long long* __restrict__ val,
+                               const unsigned long long* __restrict__ off_raw, const unsigned long long* __restrict__ off2,
+                               const unsigned long long* __restrict__ off1, uint32_t nt, uint32_t nw, uint32_t wlog,
+                               uint16_t* __restrict__ slots, uint16_t* __restrict__ offs) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += (long long)gridDim.x * blockDim.x) {
+        const uint32_t k = key[i], t = k / nw, w = k - t * nw;
+        const unsigned long long j = (unsigned long long)i - off_raw[k];
+        const unsigned long long v = val[i];
+        slots[off2[k] + j] = (uint16_t)(v & 0xfffffu);
+        offs[off1[(unsigned long long)w * nt + t] + j] = (uint16_t)((uint32_t)(v >> 20) - (w << wlog));
+    }
+}
+
+// window-order group -> tile-order group, per chunk
+__global__ void tp_gword_kernel(long long nk, const uint32_t* __restrict__ cnt, const unsigned long long* __restrict__ off2,
+                                const unsigned long long* __restrict__ off1, uint32_t nt, uint32_t nw,
+                                uint32_t* __restrict__ gword) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += (long long)gridDim.x * blockDim.x) {
+        const uint32_t ng = (cnt[k] + 31u) >> 5;
+        if (!ng) continue;
+        const uint32_t t = (uint32_t)(k / nw), w = (uint32_t)(k - (long long)t * nw);
+        const unsigned long long g2 = off2[k] >> 5, g1 = off1[(unsigned long long)w * nt + t] >> 5;
+        for (uint32_t j = 0; j < ng; ++j) gword[g1 + j] = (uint32_t)(g2 + j);
+    }
+}
+
+__global__ void fill_u16_kernel(long long n, uint16_t* p, uint16_t v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+}  // namespace snp

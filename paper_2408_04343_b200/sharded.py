@@ -103,14 +103,15 @@ class ShardedEngine:
     every edge that enters the rank's rows.
     """
 
-    def __init__(self, local: SystemArrays, q: int, rank: int, world: int, device: int = 0):
+    def __init__(self, local: SystemArrays, q: int, rank: int, world: int, device: int = 0,
+                 variant: str = "tiled"):
         self.layout = shard_layout(q, world)
         self.rank, self.world = rank, world
         self.lo, self.hi = self.layout.bounds(rank)
         if local.neuron_count != self.hi - self.lo:
             raise ValueError(f"rank {rank} owns {self.hi - self.lo} neurons, got {local.neuron_count}")
         self.engine = DeviceEngine(Format.COMPRESSED, q, local.rules, local.rule_map.offsets, local.initial,
-                                   adj=(local.adj_offsets, local.adj_targets), variant="tiled",
+                                   adj=(local.adj_offsets, local.adj_targets), variant=variant,
                                    device=device, world=world, rank=rank)
         self.x = self.engine.exchange_info()
         self._views = None

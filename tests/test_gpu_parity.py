@@ -407,3 +407,33 @@ def test_device_layout_build_matches_host(case, monkeypatch):
     assert digests[0] == digests[1]
     assert any(digests[0])
     np.testing.assert_array_equal(finals[0], finals[1])
+
+
+# -- two-pass receive (variant tiled2) -------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["synth", "synth_delays_seeded", "sort300", "sparse_far"])
+def test_tiled2_matches_oracle(case):
+    if case == "sort300":
+        a, L, sel, pol, seed = snp.sort_arrays(snp.SortInstance(300)), 310, snp.FirstApplicable(), 0, 0
+    elif case == "sparse_far":
+        a, L, sel, pol, seed = _sparse_far_system(), 20, snp.SeededRandom(3), 1, 3
+    else:
+        d = case != "synth"
+        a = snp.synth_v1(250_000, with_delays=d)
+        L, sel, pol, seed = 30, (snp.SeededRandom(9) if d else snp.FirstApplicable()), (1 if d else 0), (9 if d else 0)
+    prep = snp.prepare(a, snp.Format.COMPRESSED, variant="tiled2")
+    res = snp.run_final(prep, snp.SimOptions(max_steps=L, selection=sel))
+    _, want_c, want_d = coracle.run(OracleSystem.from_arrays(a), L, pol, seed)
+    np.testing.assert_array_equal(res.config, want_c)
+    np.testing.assert_array_equal(res.delays, want_d)
+    tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=12, selection=sel, record=snp.RecordLevel.FULL))
+    ref, _, _ = coracle.run(OracleSystem.from_arrays(a), 12, pol, seed, trace_rows=13)
+    assert trace_digest(tr.configs, tr.delays, tr.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
+
+
+@pytest.mark.parametrize("name", scenario_names())
+def test_tiled2_scenarios(name):
+    prep = snp.prepare(to_system_arrays(scenario_system(name)), snp.Format.COMPRESSED, variant="tiled2")
+    for tag, sel in POLICIES.items():
+        tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=60, selection=sel, record=snp.RecordLevel.FULL))
+        _check(tr, scenario_trace(name, tag))

@@ -327,3 +327,21 @@ def test_k5_scale_sharded_equals_single_and_oracle():
     np.testing.assert_array_equal(cfg, want3.config)
     np.testing.assert_array_equal(dly, want3.delays)
     assert steps == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_exchange_tiled2_matches_single(world, monkeypatch):
+    """Row partition with the two-pass receive (windows over the exchange space)."""
+    arrays = snp.synth_v1(80_000, with_delays=True)
+    sel = snp.SeededRandom(5)
+    want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED), snp.SimOptions(max_steps=10, selection=sel))
+    orig = shd.ShardedEngine.__init__
+
+    def init_tiled2(self, local, q, rank, world, device=0, variant="tiled"):
+        orig(self, local, q, rank, world, device, variant="tiled2")
+
+    monkeypatch.setattr(shd.ShardedEngine, "__init__", init_tiled2)
+    cfg, dly, steps, _ = _run_p2p_on_one_gpu(arrays, world, 10, sel)
+    np.testing.assert_array_equal(cfg, want.config)
+    np.testing.assert_array_equal(dly, want.delays)
