@@ -156,6 +156,8 @@ struct DevSys {
     const uint16_t* tp_off;       // [groups * 32] source offsets in the window, window order
     const uint32_t* tp_gword;     // [groups] window-order group -> tile-order group
     const uint32_t* tp_wgroup;    // [tp_nw + 1] window -> first window-order group
+    const uint4* tp_items;        // pass-1 work items {window, first group, end group, 0}
+    long long tp_nitems;
     // peer exchange (NVLink P2P): every rank's exchange block (3 slots of
     // p_words words, then `world` 64-bit step flags), mapped into this process
     const unsigned long long* peers;
@@ -1614,7 +1616,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
 // bits, stored at its tile-order position for the tiled kernel's phase 1.
 constexpr int kMaxWindowWords = (1 << 17) / 32;
 
-__global__ void __launch_bounds__(256) pass1_kernel(DevSys s, DevState st) {
+__global__ void __launch_bounds__(512) pass1_kernel(DevSys s, DevState st) {
     __shared__ uint32_t pw[kMaxWindowWords];
     __shared__ int x_ok;
     Ctrl* ctl = st.ctrl;
@@ -1629,29 +1631,42 @@ __global__ void __launch_bounds__(256) pass1_kernel(DevSys s, DevState st) {
     const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const uint32_t wwords = 1u << (s.tp_wlog - 5);
-    for (long long w = blockIdx.x; w < s.tp_nw; w += gridDim.x) {
-        const uint32_t* src = Pprev + w * wwords;
+    // work items: (window, group range) -- windows split so that items
+    // outnumber CTAs several times (balance)
+    for (long long it = blockIdx.x; it < s.tp_nitems; it += gridDim.x) {
+        const uint4 item = __ldg(s.tp_items + it);
+        const uint32_t w = item.x, g0 = item.y, g1 = item.z;
+        const uint32_t* src = Pprev + (size_t)w * wwords;
         for (uint32_t i = threadIdx.x; i < wwords; i += blockDim.x) pw[i] = __ldcg(src + i);
         __syncthreads();
-        const uint32_t g0 = __ldg(s.tp_wgroup + w), g1 = __ldg(s.tp_wgroup + w + 1);
-        uint32_t g = g0 + warp;
-        for (; g + 3u * nwarps < g1; g += 4u * nwarps) {
-            uint32_t o[4], d[4];
+        // a warp takes 8 groups (256 edges) per round, 4 rounds in flight:
+        // lane l loads 16 bytes = 8 offsets of group l / 4, makes their 8 bits,
+        // and 4 lanes OR their bytes into the group's word (lane 4j writes it)
+        const uint32_t j = lane >> 2;
+        for (uint32_t gb = g0 + 8u * warp; gb < g1; gb += 32u * nwarps) {
+            uint4 o[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                o[u] = __ldg(s.tp_off + (size_t)(g + u * nwarps) * 32 + lane);
-                d[u] = __ldg(s.tp_gword + g + u * nwarps);
+                const uint32_t gu = gb + u * 8u * nwarps;
+                o[u] = make_uint4(0, 0, 0, 0);
+                if (gu + j < g1) o[u] = __ldg(reinterpret_cast<const uint4*>(s.tp_off + (size_t)gu * 32) + lane);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const unsigned bits = __ballot_sync(0xffffffffu, (pw[o[u] >> 5] >> (o[u] & 31u)) & 1u);
-                if (lane == 0) s.tp_bits[d[u]] = bits;
+                const uint32_t gu = gb + u * 8u * nwarps;
+                const uint32_t ov[4] = {o[u].x, o[u].y, o[u].z, o[u].w};
+                uint32_t byte = 0;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const uint32_t lo = ov[x] & 0xffffu, hi = ov[x] >> 16;
+                    byte |= ((pw[lo >> 5] >> (lo & 31u)) & 1u) << (2 * x);
+                    byte |= ((pw[hi >> 5] >> (hi & 31u)) & 1u) << (2 * x + 1);
+                }
+                uint32_t word = byte << ((lane & 3u) << 3);
+                word |= __shfl_xor_sync(0xffffffffu, word, 1);
+                word |= __shfl_xor_sync(0xffffffffu, word, 2);
+                if ((lane & 3u) == 0 && gu + j < g1) s.tp_bits[__ldg(s.tp_gword + gu + j)] = word;
             }
-        }
-        for (; g < g1; g += nwarps) {
-            const uint32_t o = __ldg(s.tp_off + (size_t)g * 32 + lane);
-            const unsigned bits = __ballot_sync(0xffffffffu, (pw[o >> 5] >> (o & 31u)) & 1u);
-            if (lane == 0) s.tp_bits[__ldg(s.tp_gword + g)] = bits;
         }
         __syncthreads();
     }

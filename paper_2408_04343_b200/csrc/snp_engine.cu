@@ -275,7 +275,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     // sources spread over >= 4x this engine's rows (row partition at 4+ ranks):
     // each tile's P windows span all sources, so fewer, larger tiles read
     // fewer window bytes per edge (large systems)
-    if (per_sm == 2 && n_src >= 4 * std::max<long long>(q, 1)) per_sm = 1;
+    if (per_sm == 2 && !s.tp && n_src >= 4 * std::max<long long>(q, 1)) per_sm = 1;
     if (const char* env = getenv("SNPB200_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
     long long T = ceil_div(std::max<long long>(q, 1), per_sm * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
@@ -660,6 +660,15 @@ int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, 
     for (long long t = 0; t <= nt; ++t) tgroup[t] = (uint32_t)(off2[std::min<long long>(t * nw, nk)] / 32);
     uint32_t* d_wgroup;
     TRY(upload(e, &d_wgroup, wgroup));
+    // pass-1 work items: windows cut into runs of <= 1024 groups
+    std::vector<uint4> items;
+    for (long long w = 0; w < nw; ++w)
+        for (uint32_t g = wgroup[w]; g < wgroup[w + 1]; g += 1024)
+            items.push_back(make_uint4((uint32_t)w, g, std::min<uint32_t>(g + 1024, wgroup[w + 1]), 0));
+    uint4* d_items;
+    TRY(upload(e, &d_items, items));
+    s.tp_items = d_items;
+    s.tp_nitems = (long long)items.size();
     // stage descriptors: phase-1 runs of groups, then the phase-2 stages
     const uint32_t G = (kStageBytes - kPayload - 32) / 68;
     std::vector<StageDesc> desc;
@@ -697,7 +706,7 @@ int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, 
     s.tp_wgroup = d_wgroup;
     e->in_edges = edges;
     e->n_stages = (long long)desc.size();
-    e->p1_grid = (int)std::max<long long>(1, std::min<long long>(nw, 148ll * 8));
+    e->p1_grid = (int)std::max<long long>(1, std::min<long long>((long long)items.size(), 148ll * 4));
     return SNP_OK;
 }
 
@@ -1214,7 +1223,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
 // Two-pass receive: pass 1 (edge bits per source window) before the step kernel.
 int launch_pass1(snp_engine* e) {
     if (!e->sys.tp) return 0;
-    pass1_kernel<<<e->p1_grid, 256, 0, e->stream>>>(e->sys, e->st);
+    pass1_kernel<<<e->p1_grid, 512, 0, e->stream>>>(e->sys, e->st);
     return 1;
 }
 
