@@ -979,7 +979,11 @@ constexpr int kWarpsC = kTileThreads / 32;              // consumer warps
 constexpr uint32_t kStageBytes = SNP_STAGE_KB * 1024u;  // one ring stage
 constexpr uint32_t kHdrBytes = 512;                     // stage header (+ segment bases)
 constexpr uint32_t kMaxSegPerStage = (kHdrBytes - 32) / 4;
-constexpr int kSub = kTileThreads;                      // destinations per phase-2 stage
+#ifndef SNP_P2_REP
+#define SNP_P2_REP 1
+#endif
+constexpr int kP2Rep = SNP_P2_REP;                       // phase-2 destinations per consumer thread
+constexpr int kSub = kTileThreads * kP2Rep;             // destinations per phase-2 stage
 #ifndef SNP_SEG_SPLIT
 #define SNP_SEG_SPLIT 1
 #endif
@@ -1411,90 +1415,96 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                 const int* ds_s = reinterpret_cast<const int*>(buf + kPayload + b_cfg);
                 const uint32_t* roff_s = reinterpret_cast<const uint32_t*>(buf + kPayload + b_cfg + b_ds);
                 const Raw* rules_s = reinterpret_cast<const Raw*>(buf + kPayload + b_cfg + b_ds + b_roff);
-                const int li = threadIdx.x;
-                const int i = (int)first + li;
-                const long long j = d0 + i;
-                const bool active = li < (int)n;
-                uint32_t r0 = 0, r1 = 0;
-                long long Cprev = 0;
-                int dsv = 0;
-                if (active) {
-                    // regular systems (s.rpn rules per neuron) have implicit offsets
-                    r0 = s.rpn ? (uint32_t)(s.rpn * j) : roff_s[li];
-                    r1 = s.rpn ? r0 + (uint32_t)s.rpn : roff_s[li + 1];
-                    Cprev = cfg_s[li];
-                    dsv = ds_s[li];
-                }
-                const uint32_t nr = r1 - r0;
-                const bool heavy = active && nr > kLightRules;
-                int r = -1;
-                long long pval = 0;
                 bool released = false;
-                if (s.dbg & 2) {
-                    // timing experiment only: skip phase-2 work
-                } else if (LEAN && !WIDE && rstaged && __all_sync(0xffffffffu, !active || nr <= 4u)) {
-                    // lean fast path: <= 4 staged rule words per neuron, branch-free
-                    // selection; the stage is released once they are in registers
-                    constexpr int kW = TINY ? 4 : 8;
-                    alignas(16) uint32_t wv[kW];
+                // kP2Rep destinations per consumer thread (li, li + kTileThreads, ...)
+#pragma unroll 1
+                for (int rep = 0; rep < kP2Rep; ++rep) {
+                    const int li = threadIdx.x + rep * kTileThreads;
+                    const int i = (int)first + li;
+                    const long long j = d0 + i;
+                    const bool active = li < (int)n;
+                    uint32_t r0 = 0, r1 = 0;
+                    long long Cprev = 0;
+                    int dsv = 0;
                     if (active) {
-                        const uint32_t* rp = reinterpret_cast<const uint32_t*>(
-                            reinterpret_cast<const uint8_t*>(rules_s) + (r0 - r_al) * (TINY ? 4u : 8u));
-#pragma unroll
-                        for (int x = 0; x < kW; ++x) wv[x] = rp[x];
+                        // regular systems (s.rpn rules per neuron) have implicit offsets
+                        r0 = s.rpn ? (uint32_t)(s.rpn * j) : roff_s[li];
+                        r1 = s.rpn ? r0 + (uint32_t)s.rpn : roff_s[li + 1];
+                        Cprev = cfg_s[li];
+                        dsv = ds_s[li];
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty_bar[b]);
-                    released = true;
-                    if (active) {
+                    const uint32_t nr = r1 - r0;
+                    const bool heavy = active && nr > kLightRules;
+                    int r = -1;
+                    long long pval = 0;
+                    if (s.dbg & 2) {
+                        // timing experiment only: skip phase-2 work
+                    } else if (LEAN && !WIDE && rstaged && __all_sync(0xffffffffu, !active || nr <= 4u)) {
+                        // lean fast path: <= 4 staged rule words per neuron, branch-free
+                        // selection; the stage is released once they are in registers
+                        constexpr int kW = TINY ? 4 : 8;
+                        alignas(16) uint32_t wv[kW];
+                        if (active) {
+                            const uint32_t* rp = reinterpret_cast<const uint32_t*>(
+                                reinterpret_cast<const uint8_t*>(rules_s) + (r0 - r_al) * (TINY ? 4u : 8u));
+    #pragma unroll
+                            for (int x = 0; x < kW; ++x) wv[x] = rp[x];
+                        }
+                        if (kP2Rep == 1) {
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&empty_bar[b]);
+                            released = true;
+                        }
+                        if (active) {
+                            long long C = Cprev;
+                            if (ds_open(dsv)) {
+                                const uint32_t gsum = tile_acc_get<CB>(acc, i);
+                                C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
+                            }
+                            const int D = ds_next(dsv);
+                            pval = lean_commit4<PM, TINY>(s, st, ctl, cx, j, nr, wv, C, D, sel && D == 0, t_fired, t_closed,
+                                                          t_neg);
+                        }
+                    } else if (active) {
+                        const bool open_prev = ds_open(dsv);
+                        const int D = ds_next(dsv);
+                        const bool can_sel = sel && D == 0 && !heavy;
+                        Raw w0{}, w1{}, w2{}, w3{};
+                        if (can_sel) {
+                            if (rstaged && !TINY) {
+                                const Raw* rp = rules_s + (r0 - r_al);
+                                if (nr > 0) w0 = rp[0];
+                                if (nr > 1) w1 = rp[1];
+                                if (nr > 2) w2 = rp[2];
+                                if (nr > 3) w3 = rp[3];
+                            } else {
+                                if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                                if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                                if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                                if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                            }
+                        }
                         long long C = Cprev;
-                        if (ds_open(dsv)) {
+                        if (open_prev) {
                             const uint32_t gsum = tile_acc_get<CB>(acc, i);
                             C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
                         }
-                        const int D = ds_next(dsv);
-                        pval = lean_commit4<PM, TINY>(s, st, ctl, cx, j, nr, wv, C, D, sel && D == 0, t_fired, t_closed,
-                                                      t_neg);
+                        pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3,
+                                                                            C, D, can_sel, stat, t_fired, t_closed, t_neg,
+                                                                            neg_idx, neg_val, r);
                     }
-                } else if (active) {
-                    const bool open_prev = ds_open(dsv);
-                    const int D = ds_next(dsv);
-                    const bool can_sel = sel && D == 0 && !heavy;
-                    Raw w0{}, w1{}, w2{}, w3{};
-                    if (can_sel) {
-                        if (rstaged && !TINY) {
-                            const Raw* rp = rules_s + (r0 - r_al);
-                            if (nr > 0) w0 = rp[0];
-                            if (nr > 1) w1 = rp[1];
-                            if (nr > 2) w2 = rp[2];
-                            if (nr > 3) w3 = rp[3];
-                        } else {
-                            if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
-                            if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
-                            if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
-                            if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
-                        }
-                    }
-                    long long C = Cprev;
-                    if (open_prev) {
-                        const uint32_t gsum = tile_acc_get<CB>(acc, i);
-                        C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
-                    }
-                    pval = light_commit<RECV_PULL, PM, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3,
-                                                                        C, D, can_sel, stat, t_fired, t_closed, t_neg,
-                                                                        neg_idx, neg_val, r);
-                }
-                if (sel && PM == P_BIT) {
-                    const unsigned int bits = __ballot_sync(0xffffffffu, pval > 0);
-                    const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
-                    const unsigned int act = __ballot_sync(0xffffffffu, active);
-                    if (lane == 0 && act) {
-                        const long long wd = (j + s.xbase) >> 5;
-                        Pzero[wd] = 0u;
-                        if (hv) {
-                            if (bits) atomicOr(Pcur + wd, bits);
-                        } else {
-                            Pcur[wd] = bits;
+                    if (sel && PM == P_BIT) {
+                        const unsigned int bits = __ballot_sync(0xffffffffu, pval > 0);
+                        const unsigned int hv = __ballot_sync(0xffffffffu, heavy);
+                        const unsigned int act = __ballot_sync(0xffffffffu, active);
+                        if (lane == 0 && act) {
+                            const long long wd = (j + s.xbase) >> 5;
+                            Pzero[wd] = 0u;
+                            if (hv) {
+                                if (bits) atomicOr(Pcur + wd, bits);
+                            } else {
+                                Pcur[wd] = bits;
+                            }
                         }
                     }
                 }
