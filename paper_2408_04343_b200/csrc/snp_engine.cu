@@ -391,7 +391,6 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     // phase-2 stages kSub destinations with (when they fit) their rule words
     std::vector<StageDesc> desc;
     std::vector<uint32_t> tstage(n_tiles + 1, 0), sbases;
-    const uint32_t rw_size = e->tiny_rules ? 4u : (e->wide_rules ? 16u : 8u);
     auto r16 = [](unsigned long long x) { return (uint32_t)((x + 15) & ~15ull); };
     for (long long t = 0; t < n_tiles; ++t) {
         uint32_t g = tseg[t];
