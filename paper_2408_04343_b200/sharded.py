@@ -283,6 +283,7 @@ def bench_sharded(args, rank: int, world: int) -> None:
     forces the all-gather."""
     import json
     import os
+    import sys
     import time
 
     import torch
@@ -322,10 +323,26 @@ def bench_sharded(args, rank: int, world: int) -> None:
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     use_p2p = bool(flag.item())
     if use_p2p:
-        torch_connect_p2p(sh)
-        ex = None
-    else:
-        ex = torch_allgather_exchange(sh)
+        # map the peers' blocks; if any rank cannot (e.g. no CUDA IPC in the
+        # container) every rank rebuilds its engine and uses the all-gather
+        ok = 1
+        try:
+            handles: list = [None] * world
+            dist.all_gather_object(handles, sh.ipc_handle())
+            sh.connect_p2p(handles)
+        except Exception as exc:  # noqa: BLE001 - reported, then the NCCL path
+            print(f"[rank {rank}] peer exchange unavailable ({exc}); falling back to the NCCL all-gather",
+                  file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], device=cdev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not flag.item():
+            use_p2p = False
+            if sh.p2p:
+                sh = ShardedEngine(local, q, rank, world, device=dev)
+                sh.engine.set_stream(stream.cuda_stream)
+        dist.barrier()
+    ex = None if use_p2p else torch_allgather_exchange(sh)
     sel = FirstApplicable()
     eng = sh.engine
 
