@@ -116,6 +116,13 @@ struct DevSys {
     long long dense_ld;
     const uint32_t* heavy;    // CTA-per-neuron list
     int n_heavy;
+    // FirstApplicable guard index of the heavy-rule neurons (by heavy index):
+    // exactly-thresholds with their lowest rule, at-least thresholds with the
+    // prefix-minimum rule, each sorted by threshold
+    const uint32_t* hx_eoff;
+    const uint2* hx_e;
+    const uint32_t* hx_aoff;
+    const uint2* hx_a;
     int light_ctas;           // CTAs striding over light tiles
     int heavy_ctas;           // CTAs striding over the heavy list
     long long light_tiles;    // ceil(q / 256)
@@ -574,6 +581,37 @@ __device__ __forceinline__ uint32_t mod_upto4(unsigned long long x, uint32_t c) 
     return lo & (c - 1u);  // c = 1, 2, 4
 }
 
+// FirstApplicable over a heavy-rule neuron through its guard index: the
+// lowest rule whose guard holds for count C (local index), or -1.
+__device__ __forceinline__ int heavy_first_applicable(const DevSys& s, int h, long long C) {
+    if (C < 0) return -1;
+    const uint32_t cc = (C >> 31) != 0 ? 0x80000000u : (uint32_t)C;
+    uint32_t best = 0xffffffffu;
+    {   // exactly: threshold == cc
+        uint32_t lo = __ldg(s.hx_eoff + h), hi = __ldg(s.hx_eoff + h + 1);
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&s.hx_e[mid].x) < cc) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < __ldg(s.hx_eoff + h + 1)) {
+            const uint2 v = __ldg(&s.hx_e[lo]);
+            if (v.x == cc) best = v.y;
+        }
+    }
+    {   // at least: the last threshold <= cc carries the prefix minimum
+        const uint32_t a0 = __ldg(s.hx_aoff + h);
+        uint32_t lo = a0, hi = __ldg(s.hx_aoff + h + 1);
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&s.hx_a[mid].x) <= cc) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo > a0) best = min(best, __ldg(&s.hx_a[lo - 1].y));
+    }
+    return best == 0xffffffffu ? -1 : (int)best;
+}
+
 // Lean light-neuron tail (no recording, no counters) for <= 4 compact rule
 // words already in shared memory: the same decisions as light_commit, computed
 // branch-free on a 32-bit saturated count (thresholds are < 2^31).  A negative
@@ -800,18 +838,11 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) step_kernel(DevSys s, 
                 }
                 __syncthreads();
                 if (policy == 0) {
-                    for (uint32_t base = r0; base < r1; base += kBlock) {
-                        const uint32_t t = base + threadIdx.x;
-                        const bool ok = t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C);
-                        if (__syncthreads_or(ok)) {
-                            const unsigned int b = __ballot_sync(0xffffffffu, ok);
-                            if (lane == 0 && b)
-                                atomicMin(reinterpret_cast<unsigned int*>(&sh_pick), base + wid * 32 + __ffs(b) - 1);
-                            __syncthreads();
-                            break;
-                        }
+                    if (threadIdx.x == 0) {
+                        const int x = heavy_first_applicable(s, h, C);
+                        sh_pick = x < 0 ? -1 : (int)(r0 + x);
                     }
-                    // sh_pick starts at -1 == 0xffffffff (unsigned max)
+                    __syncthreads();
                     r = sh_pick;
                     if (threadIdx.x == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                 } else {
@@ -1527,12 +1558,8 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                     const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
                     int r = -1;
                     if (policy == 0) {
-                        for (uint32_t rb = r0; rb < r1 && r < 0; rb += 32) {
-                            const uint32_t t = rb + lane;
-                            const unsigned int bb =
-                                __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
-                            if (bb) r = (int)(rb + __ffs(bb) - 1);
-                        }
+                        const int x = heavy_first_applicable(s, (int)hh, C);
+                        r = x < 0 ? -1 : (int)(r0 + x);
                         if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                     } else {
                         uint32_t total = 0;

@@ -1067,6 +1067,41 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     TRY(upload(e, &d_heavy, heavy));
     s.heavy = d_heavy;
     s.n_heavy = (int)heavy.size();
+    // heavy-rule neurons: guard index for FirstApplicable (sorted exactly-
+    // thresholds with their lowest rule, sorted at-least thresholds with the
+    // prefix-minimum rule) -- a binary search instead of a scan over n rules
+    if (!heavy.empty()) {
+        std::vector<uint32_t> eoff(heavy.size() + 1, 0), aoff(heavy.size() + 1, 0);
+        std::vector<uint2> ev, av;
+        for (size_t h = 0; h < heavy.size(); ++h) {
+            const uint32_t i = heavy[h], a = roff[i], b = roff[i + 1];
+            std::vector<uint2> ex, al;
+            for (uint32_t r = a; r < b; ++r)
+                ((rthr[r] & kExactBit) ? ex : al).push_back(make_uint2(rthr[r] & ~kExactBit, r - a));
+            auto by_t = [](const uint2& x, const uint2& y) { return x.x < y.x || (x.x == y.x && x.y < y.y); };
+            std::sort(ex.begin(), ex.end(), by_t);
+            std::sort(al.begin(), al.end(), by_t);
+            for (size_t k = 0; k < ex.size(); ++k)
+                if (k == 0 || ex[k].x != ex[k - 1].x) ev.push_back(ex[k]);  // lowest rule per threshold
+            uint32_t pm = 0xffffffffu;
+            for (const uint2& x : al) {
+                pm = std::min(pm, x.y);
+                av.push_back(make_uint2(x.x, pm));
+            }
+            eoff[h + 1] = (uint32_t)ev.size();
+            aoff[h + 1] = (uint32_t)av.size();
+        }
+        uint32_t *d_eoff, *d_aoff;
+        uint2 *d_ev, *d_av;
+        TRY(upload(e, &d_eoff, eoff));
+        TRY(upload(e, &d_aoff, aoff));
+        TRY(upload(e, &d_ev, ev));
+        TRY(upload(e, &d_av, av));
+        s.hx_eoff = d_eoff;
+        s.hx_aoff = d_aoff;
+        s.hx_e = d_ev;
+        s.hx_a = d_av;
+    }
     // at least one (possibly all-idle) light tile so that q == 0 still runs
     // the halting decision on the device
     s.light_tiles = std::max<long long>(1, ceil_div(q, kBlock));
