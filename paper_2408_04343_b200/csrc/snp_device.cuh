@@ -1132,6 +1132,8 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
     __shared__ __align__(8) uint64_t full_bar[kMaxRing];
     __shared__ __align__(8) uint64_t empty_bar[kMaxRing];
     __shared__ __align__(16) StageDesc desc_s[32];
+    __shared__ uint32_t sh_h3[32];   // phase 3 (seeded heavy neurons): per-warp counts
+    __shared__ int sh_h3_pick;
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     const int halted = vc->halted;
@@ -1547,10 +1549,13 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
             }
             consumer_sync(kTileThreads);  // phase-2 commits visible; acc free after phase 3
 
-            // ---- phase 3: heavy-rule neurons of this tile, one warp each
+            // ---- phase 3: heavy-rule neurons of this tile: FirstApplicable one
+            // warp each (guard index); SeededRandom all consumer warps on one
+            // neuron at a time (block-wide counts over its rules)
             const uint32_t h0 = __ldg(s.theavy + tile), h1 = __ldg(s.theavy + tile + 1);
             if (sel && h1 > h0) {
-                for (uint32_t hh = h0 + warp; hh < h1; hh += kWarpsC) {
+                const bool coop = policy != 0;
+                for (uint32_t hh = coop ? h0 : h0 + warp; hh < h1; hh += coop ? 1u : (uint32_t)kWarpsC) {
                     const long long j = s.heavy[hh];
                     const int D = st.ds[j];  // phase 2 stored D_k (>= 0, not fired)
                     if (D != 0) continue;
@@ -1562,29 +1567,43 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                         r = x < 0 ? -1 : (int)(r0 + x);
                         if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                     } else {
+                        uint32_t cnt = 0;
+                        for (uint32_t t = r0 + threadIdx.x; t < r1; t += kTileThreads)
+                            cnt += guard_ok(rule_guard_word(s.rw, WIDE, t), C) ? 1u : 0u;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                        if (lane == 0) sh_h3[warp] = cnt;
+                        consumer_sync(kTileThreads);
                         uint32_t total = 0;
-                        for (uint32_t rb = r0; rb < r1; rb += 32) {
-                            const uint32_t t = rb + lane;
-                            total += __popc(
-                                __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C)));
-                        }
-                        if (lane == 0) stat[ST_SCANNED] += r1 - r0;
+                        for (int w = 0; w < kWarpsC; ++w) total += sh_h3[w];
+                        consumer_sync(kTileThreads);
+                        if (threadIdx.x == 0) stat[ST_SCANNED] += r1 - r0;
                         if (total) {
                             uint32_t want = (uint32_t)(mix64(seed, k, j + s.gbase) % total);
-                            for (uint32_t rb = r0; rb < r1; rb += 32) {
-                                const uint32_t t = rb + lane;
-                                const unsigned int bb =
-                                    __ballot_sync(0xffffffffu, t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C));
-                                const uint32_t c = __popc(bb);
+                            for (uint32_t base = r0; base < r1; base += kTileThreads) {
+                                const uint32_t t = base + threadIdx.x;
+                                const bool ok = t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C);
+                                const unsigned int bb = __ballot_sync(0xffffffffu, ok);
+                                if (lane == 0) sh_h3[warp] = __popc(bb);
+                                consumer_sync(kTileThreads);
+                                uint32_t c = 0, before = 0;
+                                for (int w = 0; w < kWarpsC; ++w) {
+                                    const uint32_t x = sh_h3[w];
+                                    before += w < warp ? x : 0u;
+                                    c += x;
+                                }
                                 if (want < c) {
-                                    r = (int)(rb + nth_set_bit(bb, want));
+                                    if (ok && before + __popc(bb & ((1u << lane) - 1u)) == want) sh_h3_pick = (int)t;
+                                    consumer_sync(kTileThreads);
+                                    r = sh_h3_pick;
                                     break;
                                 }
                                 want -= c;
+                                consumer_sync(kTileThreads);
                             }
                         }
                     }
-                    if (lane == 0) {
+                    if (coop ? threadIdx.x == 0 : lane == 0) {
                         stat[ST_OPEN] += 1;
                         if (r >= 0) {
                             const uint4 wr = load_rule<WIDE>(s.rw, r);
@@ -1612,6 +1631,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                             }
                         }
                     }
+                    if (coop) consumer_sync(kTileThreads);
                 }
                 consumer_sync(kTileThreads);
             }
