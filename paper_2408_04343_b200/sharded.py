@@ -407,7 +407,7 @@ def bench_sharded(args, rank: int, world: int) -> None:
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (synth-v1 rows per rank)",
-            "config": {"workload": f"synth-v1 q={q} ({world} x 10^7), row-partitioned",
+            "config": {"workload": f"synth-v1 q={q} ({world} x {args.q} rows), row-partitioned",
                        "exchange": "p2p (NVLink stores from the step kernel)" if use_p2p else "nccl all-gather",
                        "format": "compressed", "variant": "tiled", "policy": "first",
                        "parallelism": f"rows/{world}", "exchange_bytes_per_step": int(sh.x.slot_bytes),
