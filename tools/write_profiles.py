@@ -42,10 +42,18 @@ def launches(path):
         a[0] += 1
         a[1] += v
         a[2].append(v)
-    tot = sum(a[1] for a in agg.values()) or 1.0
-    lines = ["kernel | launches | total_us | share | per-launch us (each)"]
-    for name, (c, t, each) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    setup_marks = ("ingest_", "cub::", "tp_", "fill_", "indeg", "transpose", "build_", "digest_u32", "load_state",
+                   "widen_", "ds_to_delay")
+    step = {k: v for k, v in agg.items() if not any(m in k for m in setup_marks)}
+    setup = {k: v for k, v in agg.items() if k not in step}
+    tot = sum(a[1] for a in step.values()) or 1.0
+    lines = ["per-step kernels (share of per-step kernel time):",
+             "kernel | launches | total_us | share | per-launch us (each)"]
+    for name, (c, t, each) in sorted(step.items(), key=lambda x: -x[1][1]):
         lines.append(f"{name} | {c} | {t:.1f} | {t / tot * 100:.1f}% | " + " ".join(f"{x:.1f}" for x in each))
+    lines += ["", "engine-creation / host-API kernels (not per step):", "kernel | launches | total_us"]
+    for name, (c, t, _) in sorted(setup.items(), key=lambda x: -x[1][1]):
+        lines.append(f"{name} | {c} | {t:.1f}")
     return lines
 
 
