@@ -960,6 +960,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity), "r"(0x989680u)
         : "memory");
 }
+// Producer-side wait: plain try_wait polling (no suspend hint) so the single
+// TMA-issuing thread reacts to a freed stage without a wake-up delay.
+#ifndef SNP_PRODUCER_POLL
+#define SNP_PRODUCER_POLL 0
+#endif
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITP_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITP_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 // global -> shared bulk copy (TMA engine), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -1258,7 +1274,10 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
                         const uint32_t kind = da.x, first = da.y, n = da.z, f3 = da.w, f4 = db.x, f5 = db.y;
                         if (s.pf) prefetch_next();
                         const int b = pb;
-                        if (pround > 0) mbar_wait(&empty_bar[b], (pround - 1) & 1u);
+                        if (pround > 0) {
+                            if (SNP_PRODUCER_POLL) mbar_wait_poll(&empty_bar[b], (pround - 1) & 1u);
+                            else mbar_wait(&empty_bar[b], (pround - 1) & 1u);
+                        }
                         if (++pb == nst) {
                             pb = 0;
                             ++pround;
