@@ -437,3 +437,61 @@ def test_tiled2_scenarios(name):
     for tag, sel in POLICIES.items():
         tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=60, selection=sel, record=snp.RecordLevel.FULL))
         _check(tr, scenario_trace(name, tag))
+
+
+# -- counts beyond 2^31 (the lean guard compares a saturated 32-bit count) ----------------
+
+@pytest.mark.parametrize("fmt,variant", FORMATS + [(snp.Format.COMPRESSED, "tiled2")],
+                         ids=FMT_IDS + ["compressed-tiled2"])
+def test_huge_counts_guards(fmt, variant):
+    """Spike counts above 2^31 against thresholds near 2^31: exactly-guards
+    must not match, at-least guards must, and counts keep growing in int64."""
+    big = 2**31 + 5
+    s = snp.SNPSystem()
+    a = s.add_neuron(big)                       # never equals 2^31-1, is >= 2^31-1
+    b = s.add_neuron(2**31 - 1)                 # exactly 2^31-1 at step 0
+    c = s.add_neuron(3 * 2**31)                 # far above every threshold
+    d = s.add_neuron(0)
+    s.add_rule(a, snp.exactly(2**31 - 1), 2**31 - 1, 1, 0)
+    s.add_rule(a, snp.at_least(2**31 - 1), 3, 2, 1)
+    s.add_rule(b, snp.exactly(2**31 - 1), 2**31 - 1, 5, 0)
+    s.add_rule(b, snp.at_least(1), 1, 1, 0)
+    s.add_rule(c, snp.at_least(2**30), 2**30, 1, 2)
+    s.add_rule(d, snp.at_least(1), 1, 1, 0)
+    for x, y in [(a, d), (b, d), (c, d), (d, a), (c, a)]:
+        s.add_synapse(x, y)
+    s.validate()
+    arrays = snp.system_arrays(s)
+    prep = snp.prepare(arrays, fmt, variant=variant)
+    for pol, seed in ((0, 0), (1, 13)):
+        sel = snp.FirstApplicable() if pol == 0 else snp.SeededRandom(seed)
+        tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=12, selection=sel, record=snp.RecordLevel.FULL))
+        ref, _, _ = coracle.run(OracleSystem.from_arrays(arrays), 12, pol, seed, trace_rows=13)
+        assert trace_digest(tr.configs, tr.delays, tr.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
+        fin = snp.run_final(prep, snp.SimOptions(max_steps=12, selection=sel))  # lean instance
+        np.testing.assert_array_equal(fin.config, np.asarray(tr.configs[-1]))
+
+
+@pytest.mark.parametrize("pmax", [3, 300, 70_000])
+def test_multi_amount_production_paths(pmax):
+    """Produced amounts that differ between rules (P as u8 / u16 / u32 per
+    neuron instead of bits): tiled (global P lookups), CSR pull and push vs
+    the C oracle at 120k neurons."""
+    base = snp.synth_v1(120_000, with_delays=True)
+    r = base.rules
+    rng = np.random.default_rng(pmax)
+    firing = r.produced > 0
+    amount = rng.integers(1, pmax + 1, size=len(r.produced))
+    produced = np.where(firing, amount, 0)
+    consumed = np.where(firing, np.maximum(r.consumed, produced), r.consumed)
+    threshold = np.where(firing & ~r.is_exact, np.maximum(r.threshold, consumed), r.threshold)
+    threshold = np.where(firing & r.is_exact, consumed, threshold)
+    rules = snp.RuleVector(threshold, r.is_exact, consumed, produced, r.delay, r.neuron)
+    initial = base.initial + rng.integers(0, 3 * pmax, size=base.neuron_count)
+    a = snp.SystemArrays(initial, rules, base.rule_map, base.adj_offsets, base.adj_targets)
+    _, want_c, want_d = coracle.run(OracleSystem.from_arrays(a), 15, 1, 21)
+    for variant in ("tiled", "pull", "push"):
+        prep = snp.prepare(a, snp.Format.COMPRESSED, variant=variant)
+        res = snp.run_final(prep, snp.SimOptions(max_steps=15, selection=snp.SeededRandom(21)))
+        np.testing.assert_array_equal(res.config, want_c, err_msg=variant)
+        np.testing.assert_array_equal(res.delays, want_d, err_msg=variant)
