@@ -16,6 +16,7 @@
 #include <cerrno>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -115,18 +116,59 @@ struct snpio_model {
 
 namespace {
 
+// f(i, thread) for i in [0, n) over up to `threads` threads (contiguous ranges).
+template <class F>
+void for_each_index(size_t n, size_t threads, F&& f) {
+    threads = std::max<size_t>(1, std::min(threads, n));
+    if (threads == 1) {
+        for (size_t i = 0; i < n; ++i) f(i, 0);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < threads; ++t)
+        th.emplace_back([&, t] {
+            for (size_t i = n * t / threads, e = n * (t + 1) / threads; i < e; ++i) f(i, t);
+        });
+    for (auto& x : th) x.join();
+}
+
+// Parsed output of one text range (the whole file, or one chunk of it).
+struct Sink {
+    std::vector<long long> initial;
+    std::vector<uint32_t> owner;
+    std::vector<long long> thr, cons, prod, dly;
+    std::vector<uint8_t> exact;
+    std::vector<unsigned long long> syn;
+    long long output = -1;
+};
+
 struct Parser {
     snpio_model* m = nullptr;
+    Sink* out = nullptr;        // where rules / synapses / output go
     long long lineno = 0;
+    bool header = false, spikes = false;
+    long long count = -1;
+    int err_code = SNPIO_OK;
+    std::string err;            // message of the first error (thread-local parsing)
     std::vector<Tok> args;
 
+    int efail(int code, const char* fmt, ...) {
+        char buf[1024];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        err = buf;
+        err_code = code;
+        return code;
+    }
     int ferr(const char* fmt, ...) {
         char buf[900];
         va_list ap;
         va_start(ap, fmt);
         vsnprintf(buf, sizeof(buf), fmt, ap);
         va_end(ap);
-        return fail(SNPIO_ERR_FORMAT, "line %lld: %s", lineno, buf);
+        return efail(SNPIO_ERR_FORMAT, "line %lld: %s", lineno, buf);
     }
     // modelfile.py:151-160
     int get_int(size_t pos, const char* what, long long* v) {
@@ -137,142 +179,234 @@ struct Parser {
         return SNPIO_OK;
     }
     // modelfile.py:163-167
-    int get_index(size_t pos, long long count, long long* v) {
+    int get_index(size_t pos, long long cnt, long long* v) {
         long long x;
         if (int rc = get_int(pos, "neuron index", &x)) return rc;
-        if (x < 1 || x > count) return ferr("neuron index %lld out of range 1..%lld", x, count);
+        if (x < 1 || x > cnt) return ferr("neuron index %lld out of range 1..%lld", x, cnt);
         *v = x - 1;
         return SNPIO_OK;
     }
 
-    int run(const char* text, size_t len) {
-        bool header = false, spikes = false;
-        long long count = -1;
-        size_t i = 0;
+    // One line of modelfile.py:74-135 (raw excludes the line break).
+    int line(const char* raw, size_t raw_n) {
+        ++lineno;
+        const char* hash = (const char*)memchr(raw, '#', raw_n);
+        const size_t n = hash ? (size_t)(hash - raw) : raw_n;
+        args.clear();
+        for (size_t k = 0; k < n;) {
+            while (k < n && is_space((unsigned char)raw[k])) ++k;
+            size_t b = k;
+            while (k < n && !is_space((unsigned char)raw[k])) ++k;
+            if (k > b) args.push_back(Tok{raw + b, k - b});
+        }
+        if (args.empty()) return SNPIO_OK;
+        const Tok key = args.front();
+        args.erase(args.begin());
+        if (!header) {
+            if (!key.is("snp")) return ferr("expected 'snp <version>' header, got %s", py_repr(raw, raw_n).c_str());
+            long long ver;
+            if (int rc = get_int(0, "format version", &ver)) return rc;
+            if (ver != 1) return ferr("unsupported format version %lld", ver);
+            header = true;
+        } else if (key.is("neurons")) {
+            if (count >= 0) return ferr("duplicate 'neurons' line");
+            if (int rc = get_int(0, "neuron count", &count)) return rc;
+            if (count < 0) return ferr("neuron count must be >= 0");
+            if (count >= (1ll << 32) - 1) return ferr("neuron count %lld too large for the native parser", count);
+        } else if (key.is("spikes")) {
+            if (count < 0) return ferr("'spikes' before 'neurons'");
+            if (spikes) return ferr("duplicate 'spikes' line");
+            if ((long long)args.size() != count) return ferr("expected %lld spike counts, got %zu", count, args.size());
+            out->initial.reserve((size_t)count);
+            for (long long p = 0; p < count; ++p) {
+                long long v;
+                if (int rc = get_int((size_t)p, "spike count", &v)) return rc;
+                if (v < 0) return efail(SNPIO_ERR_MODEL, "initial spike count must be >= 0, got %lld", v);
+                out->initial.push_back(v);
+            }
+            spikes = true;
+        } else if (key.is("rule") || key.is("synapse") || key.is("output")) {
+            if (!spikes) return ferr("directive before 'spikes' line");
+            if (key.is("rule")) {
+                if (args.size() != 6) return ferr("'rule' needs 6 fields, got %zu", args.size());
+                int exact;
+                if (args[1].is("ge")) exact = 0;
+                else if (args[1].is("eq")) exact = 1;
+                else return ferr("condition kind must be 'ge' or 'eq', got %s", args[1].repr().c_str());
+                long long own = 0, t = 0, c = 0, p = 0, d = 0;
+                if (int rc = get_index(0, count, &own)) return rc;
+                if (int rc = get_int(2, "threshold", &t)) return rc;
+                // SpikeRegex (model.py:50-55)
+                if (t < 0) return efail(SNPIO_ERR_INVALID_RULE, "condition threshold must be >= 0, got %lld", t);
+                if (exact && t < 1) return efail(SNPIO_ERR_INVALID_RULE, "an exact-count condition needs threshold >= 1");
+                if (int rc = get_int(3, "consumed", &c)) return rc;
+                if (int rc = get_int(4, "produced", &p)) return rc;
+                if (int rc = get_int(5, "delay", &d)) return rc;
+                // Rule (model.py:87-106)
+                if (c < 1) return efail(SNPIO_ERR_INVALID_RULE, "a rule must consume at least one spike, got %lld", c);
+                if (p < 0) return efail(SNPIO_ERR_INVALID_RULE, "produced spike count must be >= 0, got %lld", p);
+                if (d < 0) return efail(SNPIO_ERR_INVALID_RULE, "delay must be >= 0, got %lld", d);
+                if (p == 0) {
+                    if (d != 0) return efail(SNPIO_ERR_INVALID_RULE, "a forgetting rule cannot carry a delay");
+                    if (!exact || t != c)
+                        return efail(SNPIO_ERR_INVALID_RULE, "a forgetting rule must be guarded by exactly its consumed count");
+                } else if (p > c) {
+                    return efail(SNPIO_ERR_INVALID_RULE,
+                                 "a firing rule cannot produce more than it consumes (consumed=%lld, produced=%lld)", c, p);
+                }
+                out->owner.push_back((uint32_t)own);
+                out->thr.push_back(t);
+                out->exact.push_back((uint8_t)exact);
+                out->cons.push_back(c);
+                out->prod.push_back(p);
+                out->dly.push_back(d);
+            } else if (key.is("synapse")) {
+                if (args.size() != 2) return ferr("'synapse' needs 2 fields");
+                long long a = 0, b = 0;
+                if (int rc = get_index(0, count, &a)) return rc;
+                if (int rc = get_index(1, count, &b)) return rc;
+                if (a == b) return efail(SNPIO_ERR_REFLEXIVE, "synapse (%lld, %lld) is reflexive", a, a);
+                out->syn.push_back(((unsigned long long)a << 32) | (unsigned long long)b);
+            } else {
+                if (int rc = get_index(0, count, &out->output)) return rc;
+            }
+        } else {
+            return ferr("unknown directive %s", key.repr().c_str());
+        }
+        return SNPIO_OK;
+    }
+
+    // Lines of text[i, len) until the end, an error, or (stop_after_spikes)
+    // the line after 'spikes'; returns the offset reached.
+    size_t scan(const char* text, size_t i, size_t len, bool stop_after_spikes) {
         while (i < len) {
-            // one line (str.splitlines: \r\n counts once)
             size_t e = i;
             while (e < len && !is_break((unsigned char)text[e])) ++e;
             const char* raw = text + i;
             const size_t raw_n = e - i;
-            size_t next = e;
+            size_t next = e;  // str.splitlines: \r\n counts once
             if (next < len) next += (text[next] == '\r' && next + 1 < len && text[next + 1] == '\n') ? 2 : 1;
             i = next;
-            ++lineno;
-            const char* hash = (const char*)memchr(raw, '#', raw_n);
-            const size_t n = hash ? (size_t)(hash - raw) : raw_n;
-            args.clear();
-            for (size_t k = 0; k < n;) {
-                while (k < n && is_space((unsigned char)raw[k])) ++k;
-                size_t b = k;
-                while (k < n && !is_space((unsigned char)raw[k])) ++k;
-                if (k > b) args.push_back(Tok{raw + b, k - b});
+            if (line(raw, raw_n) != SNPIO_OK) return i;
+            if (stop_after_spikes && spikes) return i;
+        }
+        return i;
+    }
+
+    int run(const char* text, size_t len) {
+        Sink main_sink;
+        out = &main_sink;
+        size_t i = scan(text, 0, len, true);
+        if (err_code) return fail(err_code, "%s", err.c_str());
+        // the rest (rules, synapses, output) in parallel chunks cut at '\n'
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const size_t rest = len - i;
+        // SNPIO_PARSE_CHUNK_BYTES: smallest chunk (tests shrink it to exercise the split)
+        size_t chunk = 1u << 20;
+        if (const char* e = getenv("SNPIO_PARSE_CHUNK_BYTES")) chunk = std::max<size_t>(1, strtoull(e, nullptr, 10));
+        const size_t nt = rest < 4 * chunk ? 1 : std::min<size_t>(hw, rest / chunk);
+        std::vector<size_t> cut(nt + 1, len);
+        cut[0] = i;
+        for (size_t c = 1; c < nt; ++c) {
+            size_t x = std::max(cut[c - 1], i + rest * c / nt);
+            while (x < len && text[x] != '\n') ++x;
+            cut[c] = x < len ? x + 1 : len;
+        }
+        // chunks count their own lines; the first failing one is re-parsed
+        // below with its absolute line number
+        std::vector<Parser> ps(nt);
+        std::vector<Sink> sinks(nt);
+        for (size_t c = 0; c < nt; ++c) {
+            ps[c].m = m;
+            ps[c].out = &sinks[c];
+            ps[c].header = header;
+            ps[c].spikes = spikes;
+            ps[c].count = count;
+            const size_t bytes = cut[c + 1] - cut[c];
+            sinks[c].syn.reserve(bytes / 16);  // growth copies cost more than untouched reserve
+        }
+        for_each_index(nt, nt, [&](size_t c, size_t) { ps[c].scan(text, cut[c], cut[c + 1], false); });
+        long long base = lineno;
+        for (size_t c = 0; c < nt; ++c) {
+            if (ps[c].err_code) {
+                Sink scratch;
+                Parser r;
+                r.m = m;
+                r.out = &scratch;
+                r.header = header;
+                r.spikes = spikes;
+                r.count = count;
+                r.lineno = base;
+                r.scan(text, cut[c], cut[c + 1], false);
+                return fail(r.err_code, "%s", r.err.c_str());
             }
-            if (args.empty()) continue;
-            const Tok key = args.front();
-            args.erase(args.begin());
-            if (!header) {
-                if (!key.is("snp"))
-                    return ferr("expected 'snp <version>' header, got %s", py_repr(raw, raw_n).c_str());
-                long long ver;
-                if (int rc = get_int(0, "format version", &ver)) return rc;
-                if (ver != 1) return ferr("unsupported format version %lld", ver);
-                header = true;
-            } else if (key.is("neurons")) {
-                if (count >= 0) return ferr("duplicate 'neurons' line");
-                if (int rc = get_int(0, "neuron count", &count)) return rc;
-                if (count < 0) return ferr("neuron count must be >= 0");
-                if (count >= (1ll << 32) - 1) return ferr("neuron count %lld too large for the native parser", count);
-            } else if (key.is("spikes")) {
-                if (count < 0) return ferr("'spikes' before 'neurons'");
-                if (spikes) return ferr("duplicate 'spikes' line");
-                if ((long long)args.size() != count)
-                    return ferr("expected %lld spike counts, got %zu", count, args.size());
-                m->initial.reserve((size_t)count);
-                for (long long p = 0; p < count; ++p) {
-                    long long v;
-                    if (int rc = get_int((size_t)p, "spike count", &v)) return rc;
-                    if (v < 0) return fail(SNPIO_ERR_MODEL, "initial spike count must be >= 0, got %lld", v);
-                    m->initial.push_back(v);
-                }
-                spikes = true;
-            } else if (key.is("rule") || key.is("synapse") || key.is("output")) {
-                if (!spikes) return ferr("directive before 'spikes' line");
-                if (key.is("rule")) {
-                    if (args.size() != 6) return ferr("'rule' needs 6 fields, got %zu", args.size());
-                    int exact;
-                    if (args[1].is("ge")) exact = 0;
-                    else if (args[1].is("eq")) exact = 1;
-                    else return ferr("condition kind must be 'ge' or 'eq', got %s", args[1].repr().c_str());
-                    long long own = 0, t = 0, c = 0, p = 0, d = 0;
-                    if (int rc = get_index(0, count, &own)) return rc;
-                    if (int rc = get_int(2, "threshold", &t)) return rc;
-                    // SpikeRegex (model.py:50-55)
-                    if (t < 0) return fail(SNPIO_ERR_INVALID_RULE, "condition threshold must be >= 0, got %lld", t);
-                    if (exact && t < 1) return fail(SNPIO_ERR_INVALID_RULE, "an exact-count condition needs threshold >= 1");
-                    if (int rc = get_int(3, "consumed", &c)) return rc;
-                    if (int rc = get_int(4, "produced", &p)) return rc;
-                    if (int rc = get_int(5, "delay", &d)) return rc;
-                    // Rule (model.py:87-106)
-                    if (c < 1) return fail(SNPIO_ERR_INVALID_RULE, "a rule must consume at least one spike, got %lld", c);
-                    if (p < 0) return fail(SNPIO_ERR_INVALID_RULE, "produced spike count must be >= 0, got %lld", p);
-                    if (d < 0) return fail(SNPIO_ERR_INVALID_RULE, "delay must be >= 0, got %lld", d);
-                    if (p == 0) {
-                        if (d != 0) return fail(SNPIO_ERR_INVALID_RULE, "a forgetting rule cannot carry a delay");
-                        if (!exact || t != c)
-                            return fail(SNPIO_ERR_INVALID_RULE, "a forgetting rule must be guarded by exactly its consumed count");
-                    } else if (p > c) {
-                        return fail(SNPIO_ERR_INVALID_RULE,
-                                    "a firing rule cannot produce more than it consumes (consumed=%lld, produced=%lld)", c, p);
-                    }
-                    m->owner.push_back((uint32_t)own);
-                    m->thr.push_back(t);
-                    m->exact.push_back((uint8_t)exact);
-                    m->cons.push_back(c);
-                    m->prod.push_back(p);
-                    m->dly.push_back(d);
-                } else if (key.is("synapse")) {
-                    if (args.size() != 2) return ferr("'synapse' needs 2 fields");
-                    long long a = 0, b = 0;
-                    if (int rc = get_index(0, count, &a)) return rc;
-                    if (int rc = get_index(1, count, &b)) return rc;
-                    if (a == b) return fail(SNPIO_ERR_REFLEXIVE, "synapse (%lld, %lld) is reflexive", a, a);
-                    m->syn.push_back(((unsigned long long)a << 32) | (unsigned long long)b);
-                } else {
-                    if (int rc = get_index(0, count, &m->output)) return rc;
-                }
-            } else {
-                return ferr("unknown directive %s", key.repr().c_str());
-            }
+            base += ps[c].lineno;
         }
         if (!header) return fail(SNPIO_ERR_FORMAT, "empty model file");
         if (count < 0 || !spikes) return fail(SNPIO_ERR_FORMAT, "model file is missing 'neurons' or 'spikes'");
-        return finish((size_t)count);
+        // rules in file order: one thread per field
+        m->initial.swap(main_sink.initial);
+        m->output = main_sink.output;
+        for (const Sink& k : sinks)
+            if (k.output >= 0) m->output = k.output;
+        auto concat = [&](auto field, auto& dstv) {
+            size_t n = 0;
+            for (Sink& k : sinks) n += (k.*field).size();
+            dstv.resize(n);
+            size_t at = 0;
+            for (Sink& k : sinks) {
+                auto& v = k.*field;
+                std::copy(v.begin(), v.end(), dstv.begin() + at);
+                at += v.size();
+                std::remove_reference_t<decltype(v)>().swap(v);
+            }
+        };
+        for_each_index(6, 6, [&](size_t f, size_t) {
+            switch (f) {
+                case 0: concat(&Sink::owner, m->owner); break;
+                case 1: concat(&Sink::thr, m->thr); break;
+                case 2: concat(&Sink::cons, m->cons); break;
+                case 3: concat(&Sink::prod, m->prod); break;
+                case 4: concat(&Sink::dly, m->dly); break;
+                default: concat(&Sink::exact, m->exact); break;
+            }
+        });
+        return finish((size_t)count, sinks);
     }
 
     // validate(): synapses -> ascending, de-duplicated CSR
-    int finish(size_t q) {
+    int finish(size_t q, std::vector<Sink>& sinks) {
         std::vector<long long>& off = m->adj_off;
         off.assign(q + 1, 0);
-        for (unsigned long long x : m->syn) off[(x >> 32) + 1]++;
+        size_t total = 0;
+        for (const Sink& k : sinks) {
+            total += k.syn.size();
+            for (unsigned long long x : k.syn) off[(x >> 32) + 1]++;
+        }
         for (size_t v = 0; v < q; ++v) off[v + 1] += off[v];
-        std::vector<uint32_t> dst(m->syn.size());
+        std::vector<uint32_t> dst(total);
         {
             std::vector<long long> cur(off.begin(), off.end() - 1);
-            for (unsigned long long x : m->syn) dst[(size_t)cur[x >> 32]++] = (uint32_t)x;
+            for (Sink& k : sinks) {
+                for (unsigned long long x : k.syn) dst[(size_t)cur[x >> 32]++] = (uint32_t)x;
+                std::vector<unsigned long long>().swap(k.syn);
+            }
         }
-        std::vector<unsigned long long>().swap(m->syn);
-        m->adj_dst.reserve(dst.size());
-        long long w = 0;
-        for (size_t v = 0; v < q; ++v) {
+        // per-neuron sort + unique, then compaction, over neuron ranges
+        const size_t nt = total < (1u << 20) ? 1 : std::max(1u, std::thread::hardware_concurrency());
+        std::vector<long long> kept(q + 1, 0);
+        for_each_index(q, nt, [&](size_t v, size_t) {
             auto b = dst.begin() + off[v], e = dst.begin() + off[v + 1];
             std::sort(b, e);
-            e = std::unique(b, e);
-            off[v] = w;
-            for (auto it = b; it != e; ++it) m->adj_dst.push_back(*it);
-            w += (long long)(e - b);
-        }
-        off[q] = w;
+            kept[v + 1] = (long long)(std::unique(b, e) - b);
+        });
+        for (size_t v = 0; v < q; ++v) kept[v + 1] += kept[v];
+        m->adj_dst.resize((size_t)kept[q]);
+        for_each_index(q, nt, [&](size_t v, size_t) {
+            std::copy(dst.begin() + off[v], dst.begin() + off[v] + (kept[v + 1] - kept[v]),
+                      m->adj_dst.begin() + kept[v]);
+        });
+        off.swap(kept);
         return SNPIO_OK;
     }
 };

@@ -106,3 +106,57 @@ def test_native_trace_writer_matches_format_trace(tmp_path):
     empty = snp.Trace(configs=[np.zeros(0, np.int64)] * 3, halt_reason=snp.HaltReason.STEP_LIMIT)
     mf.write_trace(path, empty)
     assert path.read_text() == snp.format_trace(empty) == "\n\n\n"
+
+
+def _corrupt_cases(text):
+    """Errors planted at several places of a valid model text: format, index,
+    reflexive, rule-validation and directive errors, mixed line breaks."""
+    lines = text.split("\n")
+    n = len(lines)
+    cases = []
+    for frac, bad in [(0.95, "rule 1 ge x 1 1 0"), (0.5, "synapse 1 999999999"), (0.3, "synapse 2 2"),
+                      (0.7, "rule 1 ge 1 1 2 0"), (0.8, "neurons 4"), (0.6, "bogus 1"), (0.99, "spikes 1")]:
+        ls = list(lines)
+        ls[int(n * frac)] = bad
+        cases.append("\n".join(ls))
+    # the first of two errors wins, whichever chunk it lands in
+    ls = list(lines)
+    ls[int(n * 0.9)] = "synapse 0 1"
+    ls[int(n * 0.4)] = "rule 1 eq 0 1 1 0"
+    cases.append("\n".join(ls))
+    # \r\n, lone \r, \f and \v as line breaks (str.splitlines) before the error
+    mixed = text.replace("\n", "\r\n", 200).replace("\n", "\r", 50)
+    ls = mixed.split("\n")
+    ls[int(len(ls) * 0.75)] = "\f\vsynapse 3 3"
+    cases.append("\n".join(ls))
+    return cases
+
+
+@pytest.mark.parametrize("chunk", ["64", "1000", "1048576"])
+def test_native_chunked_parse_matches_python(chunk, monkeypatch):
+    """The native parser splits the rule/synapse section into chunks parsed on
+    several threads; arrays, the first error (file order) and its line number
+    must equal the sequential Python parser's."""
+    monkeypatch.setenv("SNPIO_PARSE_CHUNK_BYTES", chunk)
+    s = snp.SNPSystem()
+    rng = np.random.default_rng(11)
+    ids = [s.add_neuron(int(rng.integers(0, 5))) for _ in range(60)]
+    for i in ids:
+        for k in range(int(rng.integers(1, 4))):
+            s.add_rule(i, snp.at_least(k + 1), k + 1, int(rng.integers(1, k + 2)), int(rng.integers(0, 2)))
+        for j in rng.choice(len(ids), size=5, replace=False):
+            if int(j) != i:
+                s.add_synapse(i, ids[int(j)])
+    s.output_neuron = ids[7]
+    text = snp.serialize_model(s.validate())
+    text += "output 3\n# trailing comment\nsynapse 4 5\n"  # later output wins
+    want = snp.system_arrays(snp.parse_model(text))
+    _same_arrays(mf.parse_model_arrays(text), want)
+    _same_arrays(mf.parse_model_arrays(text.replace("\n", "\r\n")), want)
+    for bad in _corrupt_cases(text):
+        with pytest.raises(snp.ModelError) as py_err:
+            snp.parse_model(bad)
+        with pytest.raises(snp.ModelError) as native_err:
+            mf.parse_model_arrays(bad)
+        assert type(native_err.value) is type(py_err.value)
+        assert str(native_err.value) == str(py_err.value)
