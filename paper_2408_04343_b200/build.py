@@ -9,7 +9,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 SOURCES = [PKG / "csrc" / "snp_engine.cu"]
-DEPS = SOURCES + [PKG / "csrc" / "snp_device.cuh", PKG.parent / "include" / "snpb200.h"]
+DEPS = SOURCES + [PKG / "csrc" / "snp_device.cuh", PKG / "csrc" / "snp_ingest.cuh", PKG.parent / "include" / "snpb200.h"]
 OUT = PKG / "libsnpb200.so"
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
