@@ -690,7 +690,7 @@ __device__ __forceinline__ long long lean_commit4(const DevSys& s, const DevStat
 // per-CTA end-of-step reductions are few.
 
 template <int KIND, int PM, bool CONSUME, bool FLIST, bool WIDE>
-__global__ void __launch_bounds__(kBlock, kStepMinBlocks) step_kernel(DevSys s, DevState st) {
+__global__ void __launch_bounds__(kBlock, kStepMinBlocks) step_kernel(const __grid_constant__ DevSys s, DevState st) {
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     const int halted = vc->halted;
@@ -1138,7 +1138,7 @@ struct StageDesc {
 // LEAN: no trace recording and no traffic counters (compiled out; the host
 // launches this instance only for runs with record == 0 and stats off).
 template <int PM, int RW, int CB, bool LEAN>
-__global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys s, DevState st) {
+__global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const __grid_constant__ DevSys s, DevState st) {
     constexpr bool WIDE = RW == RW_WIDE;
     constexpr bool TINY = RW == RW_TINY;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1692,7 +1692,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(DevSys
 // bits, stored at its tile-order position for the tiled kernel's phase 1.
 constexpr int kMaxWindowWords = (1 << 17) / 32;
 
-__global__ void __launch_bounds__(512) pass1_kernel(DevSys s, DevState st) {
+__global__ void __launch_bounds__(512) pass1_kernel(const __grid_constant__ DevSys s, DevState st) {
     __shared__ uint32_t pw[kMaxWindowWords];
     __shared__ int x_ok;
     Ctrl* ctl = st.ctrl;
@@ -1753,7 +1753,7 @@ __global__ void __launch_bounds__(512) pass1_kernel(DevSys s, DevState st) {
 // Thread per neuron; columns longer than kLightOut go to the heavy queue.
 
 template <bool ELL>
-__global__ void __launch_bounds__(kBlock) push_kernel(DevSys s, DevState st, long long* row_visits) {
+__global__ void __launch_bounds__(kBlock) push_kernel(const __grid_constant__ DevSys s, DevState st, long long* row_visits) {
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     if (!vc->push_armed) return;
@@ -1801,7 +1801,7 @@ __global__ void __launch_bounds__(kBlock) push_kernel(DevSys s, DevState st, lon
 
 // Warp per queued heavy column.
 template <bool ELL>
-__global__ void __launch_bounds__(kBlock) push_heavy_kernel(DevSys s, DevState st) {
+__global__ void __launch_bounds__(kBlock) push_heavy_kernel(const __grid_constant__ DevSys s, DevState st) {
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     if (!vc->push_armed) return;
@@ -1833,7 +1833,7 @@ __global__ void __launch_bounds__(kBlock) push_heavy_kernel(DevSys s, DevState s
 
 // Dense S.M (paper Alg. 3 over the fired rows only): blockIdx.x tiles 1024
 // columns (int4 per thread), blockIdx.y splits the fired-rule list.
-__global__ void __launch_bounds__(kBlock) dense_kernel(DevSys s, DevState st) {
+__global__ void __launch_bounds__(kBlock) dense_kernel(const __grid_constant__ DevSys s, DevState st) {
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     if (!vc->push_armed) return;
@@ -1869,7 +1869,7 @@ __global__ void __launch_bounds__(kBlock) dense_kernel(DevSys s, DevState st) {
 // The source-open re-check of engine.py:252/281/321 applies: a chosen rule
 // of a closed neuron is ignored.
 template <int KIND, int PM, bool CONSUME, bool FLIST>
-__global__ void prime_kernel(DevSys s, DevState st, const long long* __restrict__ C,
+__global__ void prime_kernel(const __grid_constant__ DevSys s, DevState st, const long long* __restrict__ C,
                              const long long* __restrict__ D, const long long* __restrict__ chosen) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= s.q) return;
