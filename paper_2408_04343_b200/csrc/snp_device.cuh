@@ -1335,6 +1335,11 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
         // ================= consumer warps
         int cb = 0;           // next ring stage to consume
         uint32_t cround = 0;  // completed passes over the ring
+        // phase-1 segments go to the consumer warps round-robin across stages
+        // (a stage's first segment goes to the warp after the one that took
+        // the previous stage's last), so stages holding fewer segments than
+        // there are warps -- sparse P windows -- still keep every warp busy
+        uint32_t rot = 0;
         for (long long tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
             const long long d0 = tile * T;
             const int nd = (int)min((long long)T, q - d0);
@@ -1391,7 +1396,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                 // registers; the shared atomics into the counters come after.
                 bool released = false;
                 const uint32_t units = (s.dbg & 1) ? 0u : n * kSegSplit;
-                for (uint32_t c = warp; c < units; c += kWarpsC) {
+                const uint32_t c0 = ((uint32_t)warp + kWarpsC - rot) % kWarpsC;
+                rot = (rot + units) % kWarpsC;
+                for (uint32_t c = c0; c < units; c += kWarpsC) {
                     const uint32_t i = c / kSegSplit, part = c % kSegSplit;
                     // lane l takes edges l, l+32, ...: each instruction covers 32
                     // consecutive (source-sorted) edges, so the P-bit loads hit
