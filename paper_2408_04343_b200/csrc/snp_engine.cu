@@ -306,6 +306,14 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     s.ring = (int)ring;
     if (acc_b(T) + ring * (long long)kStageBytes > budget) T = 0;
     if (T < 32) return fail(SNP_ERR_CAPACITY, "not enough shared memory for the tiled kernel");
+    if (!getenv("SNPB200_TILE") && q > T) {
+        // whole rounds: the CTA with the most tiles sets the step time, so a
+        // partial last round is spread over all CTAs (smaller tiles, same
+        // number of rounds; e.g. 10^8 neurons: 1199 -> 1332 tiles, 9 each)
+        const long long rounds = ceil_div(ceil_div(q, T), (long long)n_sm);
+        const long long T2 = (ceil_div(q, rounds * n_sm) + 31) / 32 * 32;
+        if (T2 >= 32 && T2 < T) T = T2;
+    }
     const long long n_tiles = std::max<long long>(1, ceil_div(q, T));
     s.tile = (int)T;
     s.n_tiles = n_tiles;
