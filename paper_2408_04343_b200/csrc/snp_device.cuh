@@ -1002,21 +1002,28 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // ---------------------------------------------------------------------------
 // Tiled pull step kernel (default for COMPRESSED).
 //
-// A CTA owns a tile of `s.tile` consecutive destinations.  Their in-edges are
-// stored sorted by source and cut into 256-edge segments whose sources span
-// < 2^17 (host build: build_tiles), each word = slot << 17 | (src - seg_base).
-// Warp-specialised: one producer warp streams everything the tile needs from
-// HBM through a kRingStages-deep TMA ring in shared memory (cp.async.bulk,
-// full/empty mbarriers); the consumer warps never wait on each other except
-// at the two phase boundaries of a tile:
-//   phase 1 stages: 16 segments (16 KB); each warp takes one segment, looks
-//     its sources up in P_{k-1} (consecutive lookups hit the same L1 lines)
-//     and accumulates into per-destination counters in shared memory;
-//   phase 2 stages: 1024 destinations' Ĉ, delay state and rule offsets;
-//     each thread finishes step k-1 and selects step k for two destinations.
-// Phase 3 selects for the tile's heavy-rule neurons (> 32 rules), one warp
-// each.  The ring spans tiles, so the next tile's first segments are already
-// in flight while phase 3 / phase 2 finish.
+// A CTA owns tiles of `s.tile` consecutive destinations (a whole number of
+// rounds over the 148 CTAs).  A tile's in-edges are stored sorted by source
+// and cut into 256-edge segments whose sources span < 2^kSrcBits (host or
+// device build: build_tiles / build_tiles_device), one 32-bit word per edge =
+// slot << kSrcBits | (src - seg_base).  Warp-specialised: one producer warp
+// streams everything the tile needs from HBM through an s.ring-deep ring of
+// kStageBytes stages in shared memory (cp.async.bulk, full/empty mbarriers);
+// the consumer warps never wait on each other except at the phase
+// boundaries of a tile:
+//   phase 1 stages: as many segments as fit with the P_{k-1} window their
+//     sources span (sorted sources make it contiguous); segments go to the
+//     consumer warps round-robin across stages, lane l takes edges l, l+32,
+//     ..., looks the source bit up in the staged window and adds it to the
+//     destination's 8/16/32-bit counter in shared memory (one red.shared);
+//   phase 2 stages: kSub destinations' Ĉ, delay state (rule offsets) and
+//     rule words; each consumer thread finishes step k-1 and selects step k
+//     for one destination (lean instance: branch-free over <= 4 tiny rules).
+// Phase 3 selects for the tile's heavy-rule neurons (> 32 rules): a guard
+// index for FirstApplicable, block-wide counts for SeededRandom.  The ring
+// spans tiles, so the next tile's first stages are in flight while phases
+// 2 and 3 finish.  DESIGN.md ("Tiled pull") has the measurements behind
+// each choice.
 
 constexpr int kMaxRing = 8;  // ring stages (runtime s.ring <= kMaxRing, chosen by the host)
 constexpr int kWarpsC = kTileThreads / 32;              // consumer warps
