@@ -1296,7 +1296,12 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                         h->last = kind >> 8;
                         h->first = first;
                         h->n = n;
-                        if ((kind & 0xff) == 3) {
+                        if (k == 0 && (kind & 0xff) != 2) {
+                            // step 0: nothing was emitted before it (P_{-1} = 0), so
+                            // the receive stages are not streamed; consumers see n = 0
+                            h->n = 0;
+                            mbar_expect_tx(&full_bar[b], 0);
+                        } else if ((kind & 0xff) == 3) {
                             // two-pass phase 1: first = group, n groups; slots + edge bits
                             const uint32_t sbytes = n * 64u, ga = first & ~3u, bbytes = round16((n + (first & 3u)) * 4u);
                             h->src0 = first & 3u;
