@@ -19,9 +19,13 @@ per-step working set (~1.2 GB) is ~10x the 126 MB L2, so no flush is needed.
 * e2e -- the same metric through the C ABI with HOST buffers: per step one
   snp_run(initial=pinned host config, max_steps=1) -> pinned host config, i.e.
   H2D 8q bytes + one step + D2H 8q bytes.
-* cpu_baseline / --impl reference -- the reference's numpy engine restated in
-  oracle/snp_oracle.py (VectorEngine, engine.py:192-461) with all host cores
-  as its thread-pool workers (engine.py:170-189), timed on a bounded sample.
+* cpu_baseline / --impl reference -- the reference itself (snpsim 0.1.0,
+  unmodified, installed into baseline/_ref) on the same full-size workload:
+  its simulate_prepared (engine.py:416-461) over the direct-array Prepared
+  shim, all host cores as its thread-pool workers (engine.py:170-189).
+  --impl reference times W + K full-size steps (fewer timed steps only if K
+  would not fit the time budget; never a smaller system); cpu_baseline is a
+  2-step sample plus one workers=1 step.
 
 Multi-GPU (torchrun, N>1): weak scaling -- each rank owns a 10^7-neuron row
 shard of an (N x 10^7)-neuron system; the per-step production bits are
@@ -247,14 +251,142 @@ def run_ours(args, rank: int, world: int):
     }
 
 
-# -- CPU leg -----------------------------------------------------------------------------------
+# -- CPU leg: the unmodified reference (baseline/_ref) ------------------------------------
 
-def cpu_port(args, steps: int, q: int | None = None):
-    """The reference's vectorised engine (oracle/snp_oracle.py VectorEngine)."""
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def import_reference():
+    """The reference package ``snpsim`` as installed (unmodified) into
+    baseline/_ref, or None.  Nothing of this repo is imported on that path."""
+    if not (REF_DIR / "snpsim").is_dir():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import snpsim
+    return snpsim
+
+
+class _Shim:
+    """The only system fields the reference's simulate_prepared reads
+    (engine.py:427-428): the direct-array method of SURVEY.md 8(c)."""
+
+    def __init__(self, initial):
+        self.initial_spikes = initial
+        self.neuron_count = len(initial)
+
+
+def reference_synth(snpsim, q: int, with_delays: bool, seed: int = 240804343):
+    """synth-v1 built with numpy and the reference's own
+    mix64_array (selection.py:48-62) straight into the reference's
+    RuleVector / NeuronRuleMap / SynapseMatrix (matrices.py:48-112); the same
+    system as paper_2408_04343_b200.synth_v1 (tests/test_oracle_golden.py)."""
+    from snpsim.matrices import NeuronRuleMap, RuleVector, SynapseMatrix
+    from snpsim.selection import mix64_array
+    idx = np.arange(q, dtype=np.int64)
+    h = lambda stream: mix64_array(seed, stream, idx)  # noqa: E731
+    init = (h(0) % np.uint64(8)).astype(np.int64)
+    deg, width = 16, (q - 1) // 16
+    tg = np.empty((deg, q), dtype=np.int64)
+    for k in range(deg):
+        tg[k] = (idx + 1 + k * width + (h(1 + k) % np.uint64(width)).astype(np.int64)) % q
+    tg.sort(axis=0)
+    t0 = 2 + (h(17) % np.uint64(4)).astype(np.int64)
+    t1 = 3 + (h(18) % np.uint64(6)).astype(np.int64)
+    c1 = 1 + (h(19) % t1.astype(np.uint64)).astype(np.int64)
+    t2 = 1 + (h(20) % np.uint64(5)).astype(np.int64)
+    one = np.ones(q, np.int64)
+    thr = np.stack([t0, t1, t2, one], axis=1).reshape(-1)
+    cons = np.stack([t0, c1, t2, one], axis=1).reshape(-1)
+    prod = np.tile(np.array([1, 1, 0, 1], np.int64), q)
+    exact = np.tile(np.array([True, False, True, False]), q)
+    dly = np.zeros((q, 4), np.int64)
+    if with_delays:
+        for r, stream in ((0, 21), (1, 22), (3, 23)):
+            dly[:, r] = (h(stream) % np.uint64(4)).astype(np.int64)
+    rv = RuleVector(thr, exact, cons, prod, dly.reshape(-1), np.repeat(idx, 4))
+    rm = NeuronRuleMap(np.arange(0, 4 * q + 1, 4, dtype=np.int64))
+    return init, rv, rm, SynapseMatrix(tg)
+
+
+def host_info() -> dict:
+    model, mem_gb = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem_gb = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "usable_cpus": usable, "ram_gb": mem_gb,
+            "numpy": np.__version__, "python": sys.version.split()[0]}
+
+
+class ReferenceArm:
+    """The reference's own engine (snpsim.engine.simulate_prepared,
+    engine.py:416-461, unmodified, from baseline/_ref) on the bench workload,
+    driven through the direct-array Prepared shim.  One simulate_prepared
+    call of K steps from the initial configuration is one timed run, exactly
+    how the reference's own harness times it (bench.py:80-96)."""
+
+    def __init__(self, args):
+        self.snpsim = import_reference()
+        if self.snpsim is None:
+            raise RuntimeError(f"reference not installed at {REF_DIR}")
+        S = self.snpsim
+        from snpsim import engine as ref_engine
+        q = Q_K3 if args.workload in ("k3", "k4") else args.q
+        t0 = time.perf_counter()
+        init, rv, rm, syn = reference_synth(S, q, args.workload == "k4")
+        self.gen_s = time.perf_counter() - t0
+        self.q = q
+        self.prep = ref_engine.Prepared(_Shim(init), S.Format.COMPRESSED, rv, rm, syn)
+        self.sel = S.FirstApplicable() if args.policy == "first" else S.SeededRandom(240804343)
+
+    def run(self, steps: int, workers: int) -> float:
+        """Wall seconds of one simulate_prepared run of ``steps`` steps."""
+        S = self.snpsim
+        opts = S.SimOptions(max_steps=steps, selection=self.sel, workers=workers)
+        t0 = time.perf_counter()
+        tr = S.simulate_prepared(self.prep, opts)
+        dt = time.perf_counter() - t0
+        assert tr.steps == steps, (tr.steps, steps)
+        return dt
+
+
+def cpu_reference_sample(args, steps: int = 2) -> dict:
+    """cpu_baseline of the GPU arm: the unmodified reference on the same
+    full-size workload, all host cores (plus one workers=1 step), a bounded
+    sample of ~10-30 s of CPU work."""
+    if args.workload not in ("k3", "k4") or import_reference() is None:
+        return cpu_port_sample(args, steps)
+    arm = ReferenceArm(args)
+    cores = host_info()["usable_cpus"] or 1
+    arm.run(1, cores)  # warm-up: page faults, thread pool
+    dt = arm.run(steps, cores) / steps
+    dt1 = arm.run(1, 1)
+    return {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "reference",
+            "sample": f"{steps} full steps of the same q={arm.q} system through the unmodified reference "
+                      f"(baseline/_ref snpsim {getattr(arm.snpsim, '__version__', '0.1.0')} simulate_prepared, "
+                      f"direct-array shim, workers={cores}) after 1 warm-up step",
+            "workers1_value": 1.0 / dt1, "host": host_info()}
+
+
+def cpu_port_sample(args, steps: int = 2) -> dict:
+    """Fallback when the reference is not installed: the numpy restatement
+    (oracle/snp_oracle.py VectorEngine) of the same engine."""
     from oracle.snp_oracle import OracleSystem, VectorEngine
-    arrays, _ = make_workload(args, q)
+    arrays, _ = make_workload(args)
     s = OracleSystem.from_arrays(arrays)
-    cores = os.cpu_count() or 1
+    cores = host_info()["usable_cpus"] or 1
     pol, seed = (0, 0) if args.policy == "first" else (1, 240804343)
     ve = VectorEngine(s, args.format, workers=cores)
     cfg = s.initial.copy()
@@ -262,15 +394,62 @@ def cpu_port(args, steps: int, q: int | None = None):
 
     def one_step(k, cfg, dly):
         ch = ve.sv_calc(cfg, dly, pol, seed, k)
-        nxt = ve.step(cfg, dly, ch)
-        return nxt, ve.update_delays(dly, ch)
+        return ve.step(cfg, dly, ch), ve.update_delays(dly, ch)
 
-    cfg, dly = one_step(0, cfg, dly)  # warm-up (page faults, pool start)
+    cfg, dly = one_step(0, cfg, dly)
     t0 = time.perf_counter()
     for k in range(1, steps + 1):
         cfg, dly = one_step(k, cfg, dly)
     dt = (time.perf_counter() - t0) / steps
-    return dt, cores, s.q
+    return {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
+            "sample": f"{steps} steps of the same q={s.q} system, numpy VectorEngine ({cores} workers)",
+            "host": host_info()}
+
+
+def reference_main(args, metric: str, unit: str, config: dict) -> None:
+    """bench.py --impl reference: W warm-up steps, then K timed full-size
+    steps of the unmodified reference on this box's host cores (one
+    simulate_prepared run each).  If K steps would not finish within the
+    time budget, fewer full-size steps are timed (``steps_timed``); nothing
+    is sampled at a smaller size or extrapolated."""
+    budget_s = float(os.environ.get("SNPB200_REF_BUDGET_S", "240"))
+    cores = host_info()["usable_cpus"] or 1
+    if args.workload not in ("k3", "k4") or import_reference() is None:
+        why = "reference not installed in baseline/_ref" if import_reference() is None else \
+            f"--impl reference is defined for the K3/K4 workloads (got {args.workload})"
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return
+    t0 = time.perf_counter()
+    arm = ReferenceArm(args)
+    setup_s = time.perf_counter() - t0
+    w = max(1, args.warmup)
+    t_w = arm.run(w, cores)
+    per = t_w / w
+    k = args.steps
+    left = budget_s - (time.perf_counter() - t0)
+    if k * per > left:
+        k = max(1, int(left / per))
+    dt = arm.run(k, cores)
+    v = k / dt
+    config["workload"] = f"synth-v1 q={arm.q} out-degree 16, 4 rules/neuron" + \
+        (", delays 0-3" if args.workload == "k4" else "")
+    config["q"] = arm.q
+    config["m"] = 4 * arm.q
+    line = {
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
+        "steps": args.steps, "steps_timed": k, "warmup": w, "ms_per_step": 1000.0 * dt / k,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (synth-v1 via numpy + the reference's mix64_array)", "config": config,
+        "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "reference",
+                         "sample": f"{k} full-size steps in one simulate_prepared run (after a {w}-step run), "
+                                   f"unmodified snpsim from baseline/_ref, workers={cores}",
+                         "host": host_info()},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": {"generate_and_shim": setup_s, "generate": arm.gen_s},
+        "path": "snpsim.simulate_prepared (engine.py:416-461) via Prepared(_Shim, COMPRESSED, RuleVector, "
+                "NeuronRuleMap, SynapseMatrix)",
+    }
+    print(json.dumps(line))
 
 
 def main():
@@ -293,24 +472,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return  # the CPU reference runs once, on rank 0
-        args.q = Q_K3  # the metric is quoted per 10^7 neurons whatever N is
-        # bounded sample: whole run within a few minutes
-        n = args.steps + args.warmup
-        q_s = args.q if n <= 6 else max(1_000_000, int(args.q * 6 / n) // 1000 * 1000)
-        dt, cores, qs = cpu_port(args, max(1, args.steps), q_s)
-        scale = qs / args.q
-        v = scale / dt
-        config["workload"] = f"synth-v1 q={args.q} (K3), sampled at q={qs}"
-        line = {
-            "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": config,
-            "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} steps of a q={qs} synth-v1 system, scaled by {scale:g} to q={args.q}"},
-            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line))
-        return
+        return reference_main(args, metric, unit, config)
 
     r = run_ours(args, rank, world)
     peaks = measured_peaks()
@@ -349,11 +511,7 @@ def main():
     if args.extra:
         line["extra"] = extra_measurements(args)
     if not args.no_cpu:
-        n_cpu = 2
-        dt, cores, qs = cpu_port(args, n_cpu)
-        line["cpu_baseline"] = {"value": (qs / args.q) / dt, "unit": unit, "cores": cores, "kind": "port",
-                                "sample": f"{n_cpu} steps (after 1 warm-up) of the same q={qs} system, "
-                                          f"numpy VectorEngine with {cores} thread-pool workers"}
+        line["cpu_baseline"] = cpu_reference_sample(args)
     print(json.dumps(line))
 
 

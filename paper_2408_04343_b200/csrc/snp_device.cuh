@@ -382,13 +382,12 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
         h[2] = (uint32_t)neg;
         h[3] = 0u;
         if (p2p) publish_peers(*p2p, k, v->epoch, xhdr);
-        if (!sel) {
-            v->halted = 1;
-            v->reason = HALT_STEP_LIMIT;
-        } else {
-            v->step = k + 1;
-            if (v->stats_on) v->stats[ST_STEPS] += 1;
-        }
+        // a step kernel without selection (k == max_steps) still finished
+        // step k-1 and may have seen a negative count on any rank: the next
+        // kernel decides NegativeSpikes vs STEP_LIMIT from every rank's
+        // header (tiled_step_kernel's partition check), as for any step
+        v->step = k + 1;
+        if (sel && v->stats_on) v->stats[ST_STEPS] += 1;
         v->push_armed = 0;
         __threadfence();
         return;
@@ -1189,10 +1188,13 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
             c |= h[1];
             n |= h[2];
         }
-        if (n || (!f && !c)) {
+        // step k-1 had no selection (k-1 == max_steps): STEP_LIMIT unless a
+        // rank saw a negative count when finishing step k-2
+        const bool last = k - 1 >= vc->max_steps;
+        if (n || last || (!f && !c)) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 ctl->halted = 1;
-                ctl->reason = n ? HALT_NEGATIVE : HALT_NO_APPLICABLE;
+                ctl->reason = n ? HALT_NEGATIVE : (last ? HALT_STEP_LIMIT : HALT_NO_APPLICABLE);
                 if (!n) ctl->step = k - 1;
                 ctl->neg_any = n ? 1 : 0;
                 ctl->push_armed = 0;

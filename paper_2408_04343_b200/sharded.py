@@ -63,12 +63,17 @@ def shard_layout(q: int, world: int) -> ShardLayout:
     return ShardLayout(q, world, -(-per // 128) * 128)
 
 
-def decide_halt(flags: np.ndarray) -> HaltReason | str | None:
+def decide_halt(flags: np.ndarray, last: bool = False) -> HaltReason | str | None:
     """Halting decision from the gathered per-rank flags [world, 3]
-    (fired, closed, negative) -- the rule the step kernel applies."""
+    (fired, closed, negative) of step k -- the rule the step kernel of step
+    k+1 applies.  ``last``: step k had no selection (k == max_steps); its
+    kernel only finished step k-1, so the run ends with STEP_LIMIT unless a
+    rank saw a negative count (engine.py:443-445, :263-265)."""
     f, c, n = (bool(x) for x in np.asarray(flags).any(axis=0))
     if n:
         return "negative"
+    if last:
+        return HaltReason.STEP_LIMIT
     if not f and not c:
         return HaltReason.NO_APPLICABLE_RULES
     return None
@@ -179,7 +184,9 @@ class ShardedEngine:
                 if res.halt != nat.SNP_RUNNING:
                     break
         cfg, dly = eng.read_state()
-        reason = HaltReason.STEP_LIMIT if res.halt == nat.SNP_HALT_STEP_LIMIT else HaltReason.NO_APPLICABLE_RULES
+        # poll() raised NegativeSpikes / NativeError for the other halts
+        reason = {nat.SNP_HALT_STEP_LIMIT: HaltReason.STEP_LIMIT,
+                  nat.SNP_HALT_NO_APPLICABLE: HaltReason.NO_APPLICABLE_RULES}[int(res.halt)]
         return cfg, dly, int(res.steps), reason, res.stats_dict(), k
 
 
@@ -390,7 +397,7 @@ def bench_sharded(args, rank: int, world: int) -> None:
     t0 = time.perf_counter()
     for _ in range(e2e_n):
         start_run(1, host.numpy())
-        steps(2, 0)
+        steps(3, 0)  # step 0, the finishing kernel, the halting decision
         eng.poll()
         cfg, _ = eng.read_state()
         host.numpy()[:] = cfg

@@ -40,6 +40,8 @@ def test_layout_covers_all_rows(q, world):
 
 
 def test_decide_halt_rule():
+    assert shd.decide_halt(np.array([[0, 0, 0], [0, 0, 0]]), last=True) is snp.HaltReason.STEP_LIMIT
+    assert shd.decide_halt(np.array([[0, 0, 1], [0, 0, 0]]), last=True) == "negative"
     assert shd.decide_halt(np.array([[0, 0, 0], [0, 0, 0]])) is snp.HaltReason.NO_APPLICABLE_RULES
     assert shd.decide_halt(np.array([[0, 1, 0], [0, 0, 0]])) is None
     assert shd.decide_halt(np.array([[1, 0, 0], [0, 0, 0]])) is None
@@ -83,28 +85,59 @@ def _emulated_rank_step(osys, L, rank, cfg, dsv, pbits_full, k, max_steps):
     return new_cfg, new_ds, bits, np.array([fired, closed, neg], dtype=np.int64)
 
 
-def _gloo_worker(rank, world, port, q_case, out):
+def negative_system(q: int = 2000, victim: int | None = None, consume: int = 50):
+    """synth-v1 with one neuron that fires ``at_least(1)`` consuming ``consume``
+    spikes: its count goes negative the step after it first receives one
+    (the reference raises NegativeSpikes, engine.py:263-265).  P stays one
+    bit per neuron (every sending rule produces 1)."""
+    base = snp.synth_v1(q)
+    victim = q * 3 // 4 if victim is None else victim
+    r = base.rules
+    thr, exact, cons = r.threshold.copy(), r.is_exact.copy(), r.consumed.copy()
+    prod, dly = r.produced.copy(), r.delay.copy()
+    i0 = 4 * victim
+    thr[i0:i0 + 4] = [1, 10**6, 10**6, 10**6]
+    exact[i0:i0 + 4] = [False, True, True, True]
+    cons[i0:i0 + 4] = [consume, 10**6, 10**6, 10**6]
+    prod[i0:i0 + 4] = [1, 1, 1, 1]
+    init = base.initial.copy()
+    init[victim] = 0
+    rules = snp.RuleVector(thr, exact, cons, prod, dly, r.neuron)
+    return snp.SystemArrays(init, rules, base.rule_map, base.adj_offsets, base.adj_targets)
+
+
+def negative_step(arrays) -> int:
+    """Smallest max_steps for which the C oracle raises NegativeSpikes."""
+    from oracle.snp_oracle import OracleNegative
+    osys = OracleSystem.from_arrays(arrays)
+    for L in range(1, 200):
+        try:
+            coracle.run(osys, L)
+        except OracleNegative:
+            return L
+    raise AssertionError("no negative count within 200 steps")
+
+
+def _gloo_worker(rank, world, port, q_case, max_steps, negative, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    osys = OracleSystem.from_arrays(snp.synth_v1(q_case, with_delays=True))
+    arrays = negative_system(q_case) if negative else snp.synth_v1(q_case, with_delays=True)
+    osys = OracleSystem.from_arrays(arrays)
     L = shd.shard_layout(osys.q, world)
     lo, hi = L.bounds(rank)
     cfg = osys.initial[lo:hi].copy()
     dsv = np.zeros(hi - lo, dtype=np.int64)
     width = world * (L.nl + 128)
     pbits = np.zeros(width, dtype=np.int64)
-    max_steps, k = 12, 0
+    k = 0
     while True:
         if k > 0:
-            flags = pbits_flags
-            if shd.decide_halt(flags) is not None:
-                halt = shd.decide_halt(flags)
+            # kernel k: halting decision for step k-1 from every rank's flags
+            halt = shd.decide_halt(pbits_flags, last=k - 1 >= max_steps)
+            if halt is not None:
                 break
         cfg, dsv, bits, flags_local = _emulated_rank_step(osys, L, rank, cfg, dsv, pbits, k, max_steps)
-        if k == max_steps:
-            halt = snp.HaltReason.STEP_LIMIT
-            break
         chunk = torch.zeros(L.nl + 128, dtype=torch.int64)
         chunk[:hi - lo] = torch.from_numpy(bits)
         chunk[L.nl:L.nl + 3] = torch.from_numpy(flags_local)
@@ -119,7 +152,7 @@ def _gloo_worker(rank, world, port, q_case, out):
     mine[:hi - lo] = torch.from_numpy(cfg)
     dist.all_gather(gathered, mine)
     if rank == 0:
-        out.put((np.concatenate([g.numpy() for g in gathered])[:osys.q], k, str(halt)))
+        out.put((np.concatenate([g.numpy() for g in gathered])[:osys.q], k - 1, str(halt)))
     dist.destroy_process_group()
 
 
@@ -129,23 +162,42 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2])
-def test_protocol_over_gloo_matches_oracle(world):
-    q = 600
+def _gloo_run(world, q, max_steps, negative=False):
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q, out)) for r in range(world)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q, max_steps, negative, out))
+             for r in range(world)]
     for p in procs:
         p.start()
-    final, steps, halt = out.get(timeout=300)
+    got = out.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return got
+
+
+@pytest.mark.parametrize("world", [2])
+def test_protocol_over_gloo_matches_oracle(world):
+    q = 600
+    final, steps, halt = _gloo_run(world, q, 12)
     osys = OracleSystem.from_arrays(snp.synth_v1(q, with_delays=True))
     tr, want, _ = coracle.run(osys, 12)
     np.testing.assert_array_equal(final, want)
-    assert steps == tr.n_steps
+    assert steps == tr.n_steps and halt == str(snp.HaltReason.STEP_LIMIT)
+
+
+@pytest.mark.parametrize("extra", [0, 5])
+def test_protocol_over_gloo_negative_on_last_and_mid_step(extra):
+    """A count that goes negative in the run's final step (max_steps = the
+    first step the oracle raises at) or mid-run is reported on every rank."""
+    a = negative_system(1000)
+    L = negative_step(a)
+    _, _, halt = _gloo_run(2, 1000, L + extra, negative=True)
+    assert halt == "negative"
+    # one step fewer: the count is still non-negative, the run ends at the step limit
+    _, steps, halt = _gloo_run(2, 1000, L - 1, negative=True)
+    assert halt == str(snp.HaltReason.STEP_LIMIT) and steps == L - 1
 
 
 # -- GPU: row-partitioned engines, emulated all-gather ---------------------------------------
@@ -345,3 +397,60 @@ def test_peer_exchange_tiled2_matches_single(world, monkeypatch):
     cfg, dly, steps, _ = _run_p2p_on_one_gpu(arrays, world, 10, sel)
     np.testing.assert_array_equal(cfg, want.config)
     np.testing.assert_array_equal(dly, want.delays)
+
+
+# -- GPU: NegativeSpikes in row-partitioned runs (final step and mid-run) ----------------------
+
+def _halts_of(ranks):
+    """Per-rank outcome of poll(): 'negative' or the halt code."""
+    out = []
+    for r in ranks:
+        try:
+            out.append(int(r.engine.poll().halt))
+        except snp.NegativeSpikes:
+            out.append("negative")
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("exchange", ["allgather", "p2p"])
+@pytest.mark.parametrize("extra", [0, 7])
+def test_sharded_negative_spikes_reported(world, exchange, extra):
+    a = negative_system(3000)
+    L = negative_step(a)
+    with pytest.raises(snp.NegativeSpikes):
+        snp.run_final(snp.prepare(a, snp.Format.COMPRESSED), snp.SimOptions(max_steps=L + extra))
+    q = a.neuron_count
+    lay = shd.shard_layout(q, world)
+    ranks = [shd.ShardedEngine(shd.local_arrays(a, lay, r), q, r, world) for r in range(world)]
+    if exchange == "p2p":
+        shd.ShardedEngine.connect_local(ranks)
+        stream = torch.cuda.Stream()
+        for r in ranks:
+            r.engine.set_stream(stream.cuda_stream)
+    views = [r.slots_torch() for r in ranks]
+    for max_steps, want in ((L + extra, "negative"), (L - 1, int(snp._native.SNP_HALT_STEP_LIMIT))):
+        for r in ranks:
+            r.engine.begin()
+            r.engine.configure(max_steps, snp.FirstApplicable())
+        k = 0
+        while True:
+            for r in ranks:
+                r.engine.launch_step()
+            torch.cuda.synchronize()
+            if exchange == "allgather":
+                slot = k % 3
+                for i, r in enumerate(ranks):
+                    off, nb = int(r.x.chunk_offset_bytes), int(r.x.chunk_bytes)
+                    for j in range(world):
+                        if i != j:
+                            views[j][0][slot][off:off + nb].copy_(views[i][1][slot])
+                torch.cuda.synchronize()
+            k += 1
+            halts = _halts_of(ranks)
+            assert len(set(halts)) == 1, f"ranks disagree: {halts}"
+            if halts[0] != 0:
+                break
+            assert k < max_steps + 5
+        assert halts[0] == want, (max_steps, halts)
