@@ -256,14 +256,33 @@ def run_ours(args, rank: int, world: int):
 REF_DIR = ROOT / "baseline" / "_ref"
 
 
+_REF_MOD = None
+
+
 def import_reference():
     """The reference package ``snpsim`` as installed (unmodified) into
-    baseline/_ref, or None.  Nothing of this repo is imported on that path."""
+    baseline/_ref, or None.  Nothing of this repo is imported on that path.
+    Loaded under its own name even when ``snpsim`` is already aliased in
+    this process (the conformance tests alias it to the drop-in); callers
+    reach its submodules as attributes (``snpsim.engine``, ...)."""
+    global _REF_MOD
+    if _REF_MOD is not None:
+        return _REF_MOD
     if not (REF_DIR / "snpsim").is_dir():
         return None
-    if str(REF_DIR) not in sys.path:
-        sys.path.insert(0, str(REF_DIR))
-    import snpsim
+    ours = lambda k: k == "snpsim" or k.startswith("snpsim.")  # noqa: E731
+    saved = {k: sys.modules.pop(k) for k in list(sys.modules) if ours(k)}
+    sys.path.insert(0, str(REF_DIR))
+    try:
+        import snpsim
+        loaded = [k for k in sys.modules if ours(k)]
+    finally:
+        sys.path.remove(str(REF_DIR))
+    if saved:  # put the alias back; the reference stays reachable through _REF_MOD
+        for k in loaded:
+            sys.modules.pop(k, None)
+        sys.modules.update(saved)
+    _REF_MOD = snpsim
     return snpsim
 
 
@@ -281,8 +300,8 @@ def reference_synth(snpsim, q: int, with_delays: bool, seed: int = 240804343):
     mix64_array (selection.py:48-62) straight into the reference's
     RuleVector / NeuronRuleMap / SynapseMatrix (matrices.py:48-112); the same
     system as paper_2408_04343_b200.synth_v1 (tests/test_oracle_golden.py)."""
-    from snpsim.matrices import NeuronRuleMap, RuleVector, SynapseMatrix
-    from snpsim.selection import mix64_array
+    NeuronRuleMap, RuleVector = snpsim.matrices.NeuronRuleMap, snpsim.matrices.RuleVector
+    SynapseMatrix, mix64_array = snpsim.matrices.SynapseMatrix, snpsim.selection.mix64_array
     idx = np.arange(q, dtype=np.int64)
     h = lambda stream: mix64_array(seed, stream, idx)  # noqa: E731
     init = (h(0) % np.uint64(8)).astype(np.int64)
@@ -342,7 +361,7 @@ class ReferenceArm:
         if self.snpsim is None:
             raise RuntimeError(f"reference not installed at {REF_DIR}")
         S = self.snpsim
-        from snpsim import engine as ref_engine
+        ref_engine = S.engine
         q = Q_K3 if args.workload in ("k3", "k4") else args.q
         t0 = time.perf_counter()
         init, rv, rm, syn = reference_synth(S, q, args.workload == "k4")

@@ -72,6 +72,23 @@ long long parallel_first_fail(long long n, F f) {
     return -1;
 }
 
+// CSR out-adjacency offsets (caller-built SystemArrays): offsets[0] == 0 and
+// non-decreasing, so every out-degree and the edge count offsets[q] are
+// well defined before any kernel walks them.
+int check_csr_offsets(const int64_t* off, long long q) {
+    if (q <= 0) return SNP_OK;
+    if (off[0] != 0) return fail(SNP_ERR_BAD_ARG, "adj_offsets[0] must be 0, got %lld", (long long)off[0]);
+    const long long bad = parallel_first_fail(q, [&](long long a, long long b) -> long long {
+        for (long long i = a; i < b; ++i)
+            if (off[i + 1] < off[i]) return i;
+        return -1;
+    });
+    if (bad >= 0)
+        return fail(SNP_ERR_BAD_ARG, "adj_offsets decrease at neuron %lld (%lld > %lld)", bad, (long long)off[bad],
+                    (long long)off[bad + 1]);
+    return SNP_OK;
+}
+
 using StepFn = void (*)(DevSys, DevState);
 using PrimeFn = void (*)(DevSys, DevState, const long long*, const long long*, const long long*);
 
@@ -265,6 +282,12 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
         const long long unit = e->p_mode == P_BIT ? 1 : std::max<long long>(1, e->p_max);
         long long worst = 0;
         for (uint32_t x : indeg) worst = std::max<long long>(worst, (long long)x * unit);
+        // the counters are at most 32 bits: a destination that can receive
+        // 2^32 or more in one step needs the 64-bit CSR-pull gather
+        if (worst >= (1ll << 32))
+            return fail(SNP_ERR_CAPACITY,
+                        "a neuron can receive %lld spikes in one step, beyond the tiled kernel's 32-bit receive "
+                        "counters; use variant \"pull\"", worst);
         e->cbits = worst < 256 ? 8 : (worst < 65536 ? 16 : 32);
         if (const char* env = getenv("SNPB200_COUNTER_BITS")) e->cbits = std::max(e->cbits, atoi(env));
     }
@@ -837,6 +860,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     bool have_adj = false;
     if (d->adj_offsets) {
         soff.resize(q + 1);
+        TRY(check_csr_offsets(d->adj_offsets, q));
         const long long S = q > 0 ? d->adj_offsets[q] : 0;
         if (S >= (1ll << 32) - 1) return fail(SNP_ERR_CAPACITY, "synapse count %lld exceeds uint32", S);
         sdst.resize(S);
@@ -930,6 +954,14 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                 if (nr > (long long)kLightRules) heavy_rules += nr;
             }
             e->variant = (!sh && 2 * heavy_rules > m) ? SNP_VARIANT_PULL : SNP_VARIANT_TILED;
+            // a destination that can receive >= 2^32 spikes per step (several
+            // large produced amounts) needs the 64-bit gather of the CSR pull
+            if (!sh && !pcommon && (double)pmax * (double)sdst.size() >= 4294967296.0) {
+                std::vector<uint32_t> indeg(std::max<long long>(q, 1), 0);
+                uint32_t mx = 0;
+                for (uint32_t t : sdst) mx = std::max(mx, ++indeg[t]);
+                if ((double)pmax * (double)mx >= 4294967296.0) e->variant = SNP_VARIANT_PULL;
+            }
         }
         e->kind = e->variant == SNP_VARIANT_PUSH ? RECV_ARRAY : RECV_PULL;
         e->tiled = e->variant == SNP_VARIANT_TILED || e->variant == SNP_VARIANT_TILED2;
@@ -1431,6 +1463,7 @@ int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
         sh.nl = (ceil_div(std::max<long long>(q, 1), desc->world) + 127) / 128 * 128;
         sh.lo = std::min<long long>(q, (long long)desc->rank * sh.nl);
         sh.hi = std::min<long long>(q, sh.lo + sh.nl);
+        TRY(check_csr_offsets(desc->adj_offsets, q));
         const long long S = q > 0 ? desc->adj_offsets[q] : 0;
         if (S >= (1ll << 32) - 1 || (long long)desc->world * (sh.nl + 128) >= (1ll << 32))
             return fail(SNP_ERR_CAPACITY, "row partition exceeds 32-bit exchange positions");

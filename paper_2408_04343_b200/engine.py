@@ -563,28 +563,54 @@ def run_final(prep: Prepared, options: SimOptions, collect_stats: bool = False) 
 # -- phase functions (engine.py:192-366) --------------------------------------------
 
 _PHASE_CACHE: OrderedDict = OrderedDict()
+_PHASE_CACHE_MAX = 16
 
 
-def _phase_engine(key, pinned, build):
-    """Engines for the phase functions, cached by the identity of their
-    inputs (the cached entry pins those objects, so ids cannot be reused)."""
+def _content_key(*arrays) -> str:
+    """Digest of the arrays' contents (shape, dtype, bytes): an engine built
+    from them is reused only while the inputs are unchanged, so in-place
+    edits between calls are seen, as in the reference (which recomputes
+    from the current arrays every call)."""
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    for x in arrays:
+        x = np.ascontiguousarray(x)
+        h.update(repr((x.shape, x.dtype.str)).encode())
+        h.update(memoryview(x).cast("B"))
+    return h.hexdigest()
+
+
+def _rule_arrays(rules: RuleVector) -> tuple:
+    return (rules.threshold, rules.is_exact, rules.consumed, rules.produced, rules.delay, rules.neuron)
+
+
+def _phase_engine(key, build):
+    """Engines for the phase functions, cached by the content of their inputs
+    (at most ``_PHASE_CACHE_MAX``; ``clear_phase_cache`` frees them)."""
     hit = _PHASE_CACHE.get(key)
     if hit is not None:
         _PHASE_CACHE.move_to_end(key)
-        return hit[0]
+        return hit
     eng = build()
-    _PHASE_CACHE[key] = (eng, pinned)
-    while len(_PHASE_CACHE) > 16:
+    _PHASE_CACHE[key] = eng
+    while len(_PHASE_CACHE) > _PHASE_CACHE_MAX:
         _PHASE_CACHE.popitem(last=False)
     return eng
 
 
+def clear_phase_cache() -> None:
+    """Drop the device engines cached by the phase functions (frees their
+    device memory)."""
+    _PHASE_CACHE.clear()
+
+
 def _selection_engine(rules: RuleVector, q: int, offsets: np.ndarray | None = None) -> DeviceEngine:
+    off = offsets if offsets is not None else offsets_from_owners(np.asarray(rules.neuron), q)
+
     def build():
-        off = offsets if offsets is not None else offsets_from_owners(np.asarray(rules.neuron), q)
         empty = (np.zeros(q + 1, dtype=np.int64), np.zeros(0, dtype=np.int64))
         return DeviceEngine(Format.COMPRESSED, q, rules, off, adj=empty)
-    return _phase_engine(("sel", id(rules), q), (rules,), build)
+    return _phase_engine(("sel", q, _content_key(*_rule_arrays(rules), off)), build)
 
 
 def sv_calc(config: np.ndarray, delays: np.ndarray, rules: RuleVector, rule_map: NeuronRuleMap,
@@ -600,7 +626,13 @@ def _matrix_engine(fmt: Format, matrix, rules: RuleVector, q: int) -> DeviceEngi
         kw = {"syn": matrix} if fmt is Format.COMPRESSED else (
             {"ell": matrix} if fmt is Format.ELL else {"sparse": matrix})
         return DeviceEngine(fmt, q, rules, off, **kw)
-    return _phase_engine((fmt, id(matrix), id(rules), q), (matrix, rules), build)
+    if fmt is Format.COMPRESSED:
+        mats = (matrix.target,)
+    elif fmt is Format.ELL:
+        mats = (matrix.target, matrix.amount)
+    else:
+        mats = (matrix.data,)
+    return _phase_engine((fmt, q, _content_key(*mats, *_rule_arrays(rules))), build)
 
 
 def _step(fmt: Format, state: SimState, matrix, rules: RuleVector, row_visits=None) -> np.ndarray:

@@ -29,7 +29,7 @@ def test_reference_synth_is_synth_v1(delays):
 @needs_ref
 def test_reference_arm_runs_the_reference_engine():
     """The shimmed Prepared through snpsim.simulate_prepared == the C oracle."""
-    from snpsim import engine as ref_engine
+    ref_engine = snpsim.engine
     q, steps = 3000, 6
     init, rv, rm, syn = bench.reference_synth(snpsim, q, True)
     prep = ref_engine.Prepared(bench._Shim(init), snpsim.Format.COMPRESSED, rv, rm, syn)
