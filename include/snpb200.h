@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SNPB200_ABI_VERSION 5
+#define SNPB200_ABI_VERSION 6
 
 enum {
     SNP_OK = 0,
@@ -96,7 +96,10 @@ typedef struct snp_system_desc {
     int32_t device;              /* CUDA ordinal */
     int32_t world;               /* row partition: ranks (0 or 1 = whole system) */
     int32_t rank;                /* row partition: this engine's rank */
-    int32_t reserved;
+    int32_t x_pbits;             /* row partition: P element width agreed by every rank:
+                                    1 (bits; every sending rule produces x_pmax), 8, 16 or 32;
+                                    0 = decided from this rank's own rules */
+    int64_t x_pmax;              /* row partition: largest produced amount over all ranks */
 } snp_system_desc;
 
 typedef struct snp_run_opts {
@@ -161,7 +164,15 @@ typedef struct snp_engine_info {
     int32_t ring_stages;      /* tiled: TMA ring stages in shared memory */
     int32_t counter_bits;     /* tiled: 16 or 32-bit destination counters */
     int64_t stage_bytes;      /* tiled: bytes per ring stage */
+    int32_t push_kernel;      /* ELL / COMPRESSED-push runs: SNP_PUSH_* */
+    int32_t push_tiles;       /* SNP_PUSH_BINNED: destination tiles (bins) */
 } snp_engine_info;
+
+/* snp_engine_info.push_kernel: how a push-format run steps */
+enum { SNP_PUSH_NONE = 0,      /* pull formats / dense */
+       SNP_PUSH_UNFUSED = 1,   /* step kernel + scatter kernels (heavy-rule neurons, SNPB200_PUSH=unfused) */
+       SNP_PUSH_ATOMIC = 2,    /* one kernel, L2 RED.ADD into a receive array */
+       SNP_PUSH_BINNED = 3 };  /* one kernel, deliveries binned by destination tile (ell_bin_step_kernel) */
 
 int snp_abi_version(void);
 const char *snp_last_error(void);

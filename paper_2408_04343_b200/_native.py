@@ -40,7 +40,7 @@ class SystemDesc(ctypes.Structure):
         ("ell_target", _i64p), ("ell_amount", _i64p), ("ell_rows", ctypes.c_int64),
         ("sparse_data", _i64p),
         ("device", ctypes.c_int32), ("world", ctypes.c_int32), ("rank", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("x_pbits", ctypes.c_int32), ("x_pmax", ctypes.c_int64),
     ]
 
 
@@ -73,6 +73,9 @@ class Result(ctypes.Structure):
         return {name: int(self.stats[i]) for i, name in enumerate(STAT_NAMES)}
 
 
+PUSH_KERNELS = {0: "none", 1: "unfused", 2: "atomic", 3: "binned"}
+
+
 class EngineInfo(ctypes.Structure):
     _fields_ = [
         ("q", ctypes.c_int64), ("m", ctypes.c_int64), ("z", ctypes.c_int64),
@@ -81,6 +84,7 @@ class EngineInfo(ctypes.Structure):
         ("in_edges", ctypes.c_int64), ("p_common", ctypes.c_int64),
         ("tile", ctypes.c_int64), ("n_tiles", ctypes.c_int64),
         ("ring_stages", ctypes.c_int32), ("counter_bits", ctypes.c_int32), ("stage_bytes", ctypes.c_int64),
+        ("push_kernel", ctypes.c_int32), ("push_tiles", ctypes.c_int32),
     ]
 
 

@@ -65,7 +65,7 @@ constexpr uint32_t kDummyEdge = 0xffffffffu;  // CSR / legacy padding marker
 constexpr int kMaxTile = (1 << kDstBits) - 32;
 enum RecvKind { RECV_PULL = 0, RECV_ARRAY = 1 };
 enum Rec { REC_CONFIGS = 1, REC_DELAYS = 2, REC_SPIKING = 4 };
-enum Halt { RUNNING = 0, HALT_STEP_LIMIT = 1, HALT_NO_APPLICABLE = 2, HALT_NEGATIVE = 3, HALT_EXCHANGE = 4 };
+enum Halt { RUNNING = 0, HALT_STEP_LIMIT = 1, HALT_NO_APPLICABLE = 2, HALT_NEGATIVE = 3, HALT_EXCHANGE = 4, HALT_FAULT = 5 };
 enum Stat { ST_STEPS = 0, ST_SCANNED, ST_FIRED, ST_SENDING, ST_EDGES, ST_ROWS, ST_OPEN, ST_COUNT };
 
 // Run-control block in device memory.  Written by the last CTA of each
@@ -93,6 +93,7 @@ struct Ctrl {
     unsigned int list_count[2];   // dense fired-rule list, by step parity
     unsigned int heavy_count[2];  // push heavy queue, by step parity
     unsigned long long epoch;     // peer exchange: run number (snp_begin), high half of step flags
+    int fault;                    // sticky internal error (binned push: a bin region overflowed)
 };
 
 struct StageDesc;
@@ -144,8 +145,9 @@ struct DevSys {
     int dbg;                    // timing experiments (SNPB200_DEBUG_SKIP): 1 skip phase-1 math, 2 skip phase 2
     long long n_tiles;
     // row partition (sharded.py): local neuron j is global neuron gbase + j and
-    // publishes its P bit at exchange-space position xbase + j; rank r's chunk
-    // is x_stride words, the last 4 of which carry its step flags
+    // publishes its P element (bit / u8 / u16 / u32) at exchange-space
+    // position xbase + j; rank r's chunk is x_stride words, the last 4 of
+    // which carry its step flags
     long long gbase;
     long long xbase;
     long long x_stride;         // words per rank chunk (0 = not sharded)
@@ -170,6 +172,13 @@ struct DevSys {
     const unsigned long long* peers;
     long long p_words;
     int p2p;
+    // binned push (ell_bin_step_kernel): destination tiles of bin_T, each with
+    // a bin region [bin_off[t], bin_off[t] + bin_cap[t]) per step parity
+    int bin_T;
+    int bin_ntiles;
+    unsigned long long bin_magic;  // ceil(2^64 / bin_T): floor(x / bin_T) = umul64hi(x, bin_magic) for x < 2^31
+    int bin_amount;                // UNIT entries: the common amount of every delivery
+    const uint32_t* bin_off;       // [ntiles + 1] region starts (entries, multiples of 8)
 };
 
 struct DevState {
@@ -178,6 +187,9 @@ struct DevState {
     int* chosen;              // [q] chosen rule (push/dense formats, phase API)
     uint32_t* P[3];           // pull exchange vectors (triple buffered)
     long long* recv;          // push/dense accumulation
+    void* rbuf[2];            // fused push (push_step_kernel): receive buffers by step parity, int32 or int64
+    void* bins[2];            // binned push: bin entries by step parity (u16 slots or u32 slot|amount)
+    uint32_t* bin_fill[2];    // binned push: entries written into each tile's region, by step parity
     uint32_t* list[2];        // fired rules (dense) / heavy queue (push), by parity
     Ctrl* ctrl;
     long long* tr_cfg;        // [tr_rows][q]
@@ -317,7 +329,7 @@ constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
 // Wait until every rank has published step `kdone` (its P chunk and header
 // are in this rank's slot kdone % 3).  Returns false on timeout.
-__device__ __noinline__ bool wait_peers(const DevSys& s, unsigned long long epoch, long long kdone) {
+static __device__ __noinline__ bool wait_peers(const DevSys& s, unsigned long long epoch, long long kdone) {
     const unsigned long long want = step_tag(epoch, kdone);
     const unsigned long long* fl = peer_flags(s, s.rank);
     const unsigned long long t0 = globaltimer_ns();
@@ -332,7 +344,7 @@ __device__ __noinline__ bool wait_peers(const DevSys& s, unsigned long long epoc
 
 // Last CTA of a peer-exchange step: this rank's header words (already in its
 // own slot) go to every peer, then the step flag (release) to every rank.
-__device__ __noinline__ void publish_peers(const DevSys& s, long long k, unsigned long long epoch, const uint32_t* hdr) {
+static __device__ __noinline__ void publish_peers(const DevSys& s, long long k, unsigned long long epoch, const uint32_t* hdr) {
     const long long slot = k % 3;
     const long long hw = (long long)s.rank * s.x_stride + s.x_stride - 4;
     for (int r = 0; r < s.world; ++r) {
@@ -392,7 +404,10 @@ __device__ __forceinline__ void finish_step(Ctrl* ctl, long long k, bool sel, bo
         __threadfence();
         return;
     }
-    if (neg) {
+    if (v->fault) {
+        v->halted = 1;
+        v->reason = HALT_FAULT;
+    } else if (neg) {
         v->halted = 1;
         v->reason = HALT_NEGATIVE;
     } else if (!sel) {
@@ -609,6 +624,81 @@ __device__ __forceinline__ int heavy_first_applicable(const DevSys& s, int h, lo
         if (lo > a0) best = min(best, __ldg(&s.hx_a[lo - 1].y));
     }
     return best == 0xffffffffu ? -1 : (int)best;
+}
+
+// Warp-cooperative 32-ary search over sorted guard keys [lo, hi): the number
+// of keys with x < v (UPPER = false) or x <= v (UPPER = true).  Each round
+// the 32 lanes probe 32 evenly spaced keys with one load, so a 4096-key
+// index takes 3 dependent loads instead of 12.  All lanes return the result.
+template <bool UPPER>
+__device__ __forceinline__ uint32_t warp_bound(const uint2* __restrict__ keys, uint32_t lo, uint32_t hi, uint32_t v,
+                                               int lane) {
+    uint32_t len = hi - lo;
+    while (len > 32) {
+        const uint32_t step = (len + 31u) >> 5;
+        const uint32_t idx = lo + (uint32_t)(lane + 1) * step - 1u;
+        bool below = false;
+        if (idx < lo + len) {
+            const uint32_t x = __ldg(&keys[idx].x);
+            below = UPPER ? x <= v : x < v;
+        }
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, below));
+        const uint32_t nlo = lo + c * step;
+        const uint32_t nhi = min(lo + len, lo + (c + 1u) * step - 1u);
+        lo = nlo;
+        len = nhi - nlo;
+    }
+    bool below = false;
+    if ((uint32_t)lane < len) {
+        const uint32_t x = __ldg(&keys[lo + lane].x);
+        below = UPPER ? x <= v : x < v;
+    }
+    return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
+// heavy_first_applicable, one warp (all lanes get the answer).
+__device__ __forceinline__ int heavy_first_applicable_warp(const DevSys& s, int h, long long C, int lane) {
+    if (C < 0) return -1;
+    const uint32_t cc = (C >> 31) != 0 ? 0x80000000u : (uint32_t)C;
+    uint32_t best = 0xffffffffu;
+    {   // exactly: the first threshold >= cc, if it equals cc
+        const uint32_t e0 = __ldg(s.hx_eoff + h), e1 = __ldg(s.hx_eoff + h + 1);
+        const uint32_t i = warp_bound<false>(s.hx_e, e0, e1, cc, lane);
+        if (i < e1) {
+            const uint2 v = __ldg(&s.hx_e[i]);
+            if (v.x == cc) best = v.y;
+        }
+    }
+    {   // at least: the last threshold <= cc carries the prefix minimum
+        const uint32_t a0 = __ldg(s.hx_aoff + h), a1 = __ldg(s.hx_aoff + h + 1);
+        const uint32_t i = warp_bound<true>(s.hx_a, a0, a1, cc, lane);
+        if (i > a0) best = min(best, __ldg(&s.hx_a[i - 1].y));
+    }
+    return best == 0xffffffffu ? -1 : (int)best;
+}
+
+// SeededRandom over a heavy-rule neuron, one warp: count the applicable
+// rules, then take the (mix64 % count)-th in index order (choose_index,
+// selection.py:66-71).  Returns the global rule id or -1 (all lanes).
+template <bool WIDE>
+__device__ __forceinline__ int heavy_seeded_warp(const DevSys& s, uint32_t r0, uint32_t r1, long long C,
+                                                 unsigned long long seed, long long k, long long jg, int lane) {
+    uint32_t cnt = 0;
+#pragma unroll 4
+    for (uint32_t t = r0 + lane; t < r1; t += 32) cnt += guard_ok(rule_guard_word(s.rw, WIDE, t), C) ? 1u : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (cnt == 0) return -1;
+    uint32_t want = (uint32_t)(mix64(seed, k, jg) % cnt);
+    for (uint32_t base = r0; base < r1; base += 32) {
+        const uint32_t t = base + lane;
+        const bool ok = t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C);
+        const uint32_t b = __ballot_sync(0xffffffffu, ok);
+        const uint32_t c = __popc(b);
+        if (want < c) return (int)(base + nth_set_bit(b, want));
+        want -= c;
+    }
+    return -1;  // not reached
 }
 
 // Lean light-neuron tail (no recording, no counters) for <= 4 compact rule
@@ -837,9 +927,9 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) step_kernel(const __gr
                 }
                 __syncthreads();
                 if (policy == 0) {
-                    if (threadIdx.x == 0) {
-                        const int x = heavy_first_applicable(s, h, C);
-                        sh_pick = x < 0 ? -1 : (int)(r0 + x);
+                    if (threadIdx.x < 32) {
+                        const int x = heavy_first_applicable_warp(s, h, C, lane);
+                        if (lane == 0) sh_pick = x < 0 ? -1 : (int)(r0 + x);
                     }
                     __syncthreads();
                     r = sh_pick;
@@ -1154,8 +1244,6 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
     __shared__ __align__(8) uint64_t full_bar[kMaxRing];
     __shared__ __align__(8) uint64_t empty_bar[kMaxRing];
     __shared__ __align__(16) StageDesc desc_s[32];
-    __shared__ uint32_t sh_h3[32];   // phase 3 (seeded heavy neurons): per-warp counts
-    __shared__ int sh_h3_pick;
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
     const int halted = vc->halted;
@@ -1589,61 +1677,27 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
             }
             consumer_sync(kTileThreads);  // phase-2 commits visible; acc free after phase 3
 
-            // ---- phase 3: heavy-rule neurons of this tile: FirstApplicable one
-            // warp each (guard index); SeededRandom all consumer warps on one
-            // neuron at a time (block-wide counts over its rules)
+            // ---- phase 3: heavy-rule neurons of this tile (> 32 rules, e.g. the
+            // sorter's detectors), one warp each: FirstApplicable through the
+            // guard index (32-ary warp search), SeededRandom by two warp scans
             const uint32_t h0 = __ldg(s.theavy + tile), h1 = __ldg(s.theavy + tile + 1);
             if (sel && h1 > h0) {
-                const bool coop = policy != 0;
-                for (uint32_t hh = coop ? h0 : h0 + warp; hh < h1; hh += coop ? 1u : (uint32_t)kWarpsC) {
+                for (uint32_t hh = h0 + warp; hh < h1; hh += (uint32_t)kWarpsC) {
                     const long long j = s.heavy[hh];
                     const int D = st.ds[j];  // phase 2 stored D_k (>= 0, not fired)
                     if (D != 0) continue;
                     const long long C = st.cfg[j];
                     const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
-                    int r = -1;
+                    int r;
                     if (policy == 0) {
-                        const int x = heavy_first_applicable(s, (int)hh, C);
+                        const int x = heavy_first_applicable_warp(s, (int)hh, C, lane);
                         r = x < 0 ? -1 : (int)(r0 + x);
                         if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                     } else {
-                        uint32_t cnt = 0;
-                        for (uint32_t t = r0 + threadIdx.x; t < r1; t += kTileThreads)
-                            cnt += guard_ok(rule_guard_word(s.rw, WIDE, t), C) ? 1u : 0u;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-                        if (lane == 0) sh_h3[warp] = cnt;
-                        consumer_sync(kTileThreads);
-                        uint32_t total = 0;
-                        for (int w = 0; w < kWarpsC; ++w) total += sh_h3[w];
-                        consumer_sync(kTileThreads);
-                        if (threadIdx.x == 0) stat[ST_SCANNED] += r1 - r0;
-                        if (total) {
-                            uint32_t want = (uint32_t)(mix64(seed, k, j + s.gbase) % total);
-                            for (uint32_t base = r0; base < r1; base += kTileThreads) {
-                                const uint32_t t = base + threadIdx.x;
-                                const bool ok = t < r1 && guard_ok(rule_guard_word(s.rw, WIDE, t), C);
-                                const unsigned int bb = __ballot_sync(0xffffffffu, ok);
-                                if (lane == 0) sh_h3[warp] = __popc(bb);
-                                consumer_sync(kTileThreads);
-                                uint32_t c = 0, before = 0;
-                                for (int w = 0; w < kWarpsC; ++w) {
-                                    const uint32_t x = sh_h3[w];
-                                    before += w < warp ? x : 0u;
-                                    c += x;
-                                }
-                                if (want < c) {
-                                    if (ok && before + __popc(bb & ((1u << lane) - 1u)) == want) sh_h3_pick = (int)t;
-                                    consumer_sync(kTileThreads);
-                                    r = sh_h3_pick;
-                                    break;
-                                }
-                                want -= c;
-                                consumer_sync(kTileThreads);
-                            }
-                        }
+                        r = heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane);
+                        if (lane == 0) stat[ST_SCANNED] += r1 - r0;
                     }
-                    if (coop ? threadIdx.x == 0 : lane == 0) {
+                    if (lane == 0) {
                         stat[ST_OPEN] += 1;
                         if (r >= 0) {
                             const uint4 wr = load_rule<WIDE>(s.rw, r);
@@ -1671,7 +1725,6 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                             }
                         }
                     }
-                    if (coop) consumer_sync(kTileThreads);
                 }
                 consumer_sync(kTileThreads);
             }
@@ -1679,7 +1732,8 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                 // peer exchange: this tile's final P words (phase 2 + 3) straight
                 // into every peer's slot k % 3 -- NVLink stores that overlap the
                 // next tile's phases
-                const long long wb = (d0 + s.xbase) >> 5, we = (d0 + nd + s.xbase + 31) >> 5;
+                constexpr int kPS = PM == P_BIT ? 5 : (PM == P_U8 ? 2 : (PM == P_U16 ? 1 : 0));  // log2 P per word
+                const long long wb = (d0 + s.xbase) >> kPS, we = (d0 + nd + s.xbase + (1 << kPS) - 1) >> kPS;
                 const int nw = (int)(we - wb);
                 for (int i = threadIdx.x; i < nw * s.world; i += kTileThreads) {
                     const int r = i / nw, w = i - r * nw;
@@ -1707,12 +1761,23 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
 }
 
 // ---------------------------------------------------------------------------
+// The tiled kernel's instances live in their own translation units, one per
+// P mode (snp_tiled.cu, compiled with -DSNP_TILED_PM=0..3 in parallel).
+using TiledFn = void (*)(DevSys, DevState);
+template <int PM>
+void tiled_fns(int rw, int cb, TiledFn* step, TiledFn* lean);
+template <> void tiled_fns<P_BIT>(int, int, TiledFn*, TiledFn*);
+template <> void tiled_fns<P_U8>(int, int, TiledFn*, TiledFn*);
+template <> void tiled_fns<P_U16>(int, int, TiledFn*, TiledFn*);
+template <> void tiled_fns<P_U32>(int, int, TiledFn*, TiledFn*);
+
 // Two-pass receive, pass 1 (variant TILED2): one CTA per source window.  The
 // window's P_{k-1} bits (<= 2^17 sources, 16 KB) are read once into shared
 // memory; each group of 32 in-edges (window order) becomes one word of edge
 // bits, stored at its tile-order position for the tiled kernel's phase 1.
 constexpr int kMaxWindowWords = (1 << 17) / 32;
 
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void __launch_bounds__(512) pass1_kernel(const __grid_constant__ DevSys s, DevState st) {
     __shared__ uint32_t pw[kMaxWindowWords];
     __shared__ int x_ok;
@@ -1768,6 +1833,7 @@ __global__ void __launch_bounds__(512) pass1_kernel(const __grid_constant__ DevS
         __syncthreads();
     }
 }
+#endif  // SNP_TEMPLATES_ONLY
 
 // ---------------------------------------------------------------------------
 // Push scatter (paper Alg. 4 ELL / Alg. 5 Optimized) for step k = step-1.
@@ -1852,8 +1918,429 @@ __global__ void __launch_bounds__(kBlock) push_heavy_kernel(const __grid_constan
     if (vc->stats_on && lane == 0 && edges) atomicAdd(&ctl->stats[ST_EDGES], edges);
 }
 
+// ---------------------------------------------------------------------------
+// Fused push step (runs of ELL / COMPRESSED-push systems whose neurons all
+// have <= 32 rules): ONE kernel per step that finishes step k-1 from the
+// receive buffer of parity k&1, selects step k's rules, and scatters the
+// chosen columns into the buffer of parity (k+1)&1 -- paper Alg. 4 (ELL,
+// engine.py:269-310) / Alg. 5 (Optimized push, engine.py:313-355).
+//
+// The column walk is warp-cooperative: the fired lanes' columns are laid end
+// to end in 16-byte chunks (ELL: 2 (target, amount) pairs; Optimized: one
+// 4-byte target per lane) and each round the 32 lanes take 32 consecutive
+// chunks, finding their column by a branch-free binary search over the
+// warp's inclusive chunk prefix.  Reads are coalesced 128-bit loads with an
+// L2 evict-first hint (the columns are streamed once per step), so the
+// receive buffers (int32 when no neuron can receive 2^31 per step) stay
+// L2-resident for the RED.ADDs.  Row 0 of an ELL column is the owner's
+// consumption (owner, -c): it travels through the receive buffer like any
+// delivery and is gated by the owner's open flag at the destination, as in
+// the reference walk.
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int4 ld_stream16(const void* p, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_stream4(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <bool R64>
+__device__ __forceinline__ void recv_add(void* buf, int t, int v) {
+    if (R64) atomicAdd(reinterpret_cast<unsigned long long*>(buf) + t, (unsigned long long)(long long)v);
+    else atomicAdd(reinterpret_cast<int*>(buf) + t, v);
+}
+
+template <bool ELL, bool WIDE, bool R64>
+__global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const __grid_constant__ DevSys s, DevState st) {
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    const int halted = vc->halted;
+    const long long k = vc->step;
+    if (halted || k >= vc->stop_at) return;
+    const bool sel = k < vc->max_steps;
+    const int record = vc->record;
+    const bool stats_on = vc->stats_on != 0;
+    const long long q = s.q;
+    const StepCtx cx{k, k - vc->trace_base, q, vc->seed, nullptr, vc->policy, record, sel, stats_on};
+    void* rcur = (k & 1) ? st.rbuf[1] : st.rbuf[0];
+    void* rnext = (k & 1) ? st.rbuf[0] : st.rbuf[1];
+    const uint64_t pol = evict_first_policy();
+    const int lane = threadIdx.x & 31;
+
+    unsigned int stat[ST_COUNT];
+#pragma unroll
+    for (int i = 0; i < ST_COUNT; ++i) stat[i] = 0;
+    bool t_fired = false, t_closed = false, t_neg = false;
+    long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
+    unsigned long long edges = 0;
+
+    for (long long tile = blockIdx.x; tile < s.light_tiles; tile += gridDim.x) {
+        const long long j = tile * kBlock + threadIdx.x;
+        int r = -1;
+        long long pval = 0;
+        if (j < q) {
+            const uint32_t r0 = __ldg(s.roff + j), nr = __ldg(s.roff + j + 1) - r0;
+            const long long Cprev = st.cfg[j];
+            const int dsv = st.ds[j];
+            const bool open_prev = ds_open(dsv);
+            const int D = ds_next(dsv);
+            const bool can_sel = sel && D == 0;
+            using Raw = typename RuleRaw<WIDE>::T;
+            Raw w0{}, w1{}, w2{}, w3{};
+            if (can_sel) {
+                if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+            }
+            long long rv;
+            if (R64) {
+                long long* b = reinterpret_cast<long long*>(rcur) + j;
+                rv = *b;
+                if (rv != 0) *b = 0;
+            } else {
+                int* b = reinterpret_cast<int*>(rcur) + j;
+                rv = *b;
+                if (rv != 0) *b = 0;
+            }
+            const long long C = Cprev + (open_prev ? rv : 0);
+            // no chosen / P stores: the column is pushed right here
+            pval = light_commit<RECV_PULL, P_BIT, !ELL, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D,
+                                                                     can_sel, stat, t_fired, t_closed, t_neg, neg_idx,
+                                                                     neg_val, r);
+        }
+        // this lane's column: chunk count and start
+        uint32_t nch = 0, len = 0;
+        long long base = 0;
+        if (sel && r >= 0) {
+            if (ELL) {
+                len = __ldg(s.ell_len + r);
+                nch = (len + 1) >> 1;
+                base = (long long)r * s.ell_ld;  // in pairs (ell_ld even: 16-byte aligned)
+            } else if (pval > 0) {
+                const uint32_t e0 = __ldg(s.soff + j);
+                len = __ldg(s.soff + j + 1) - e0;
+                nch = len;
+                base = e0;
+            }
+            edges += len;
+        }
+        uint32_t incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - nch;
+        const int amount = (int)pval;
+        for (uint32_t g0 = 0; g0 < total; g0 += 32) {
+            const uint32_t g = g0 + lane;
+            int L = 0;
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, L + w - 1);
+                if (v <= g) L += w;
+            }
+            const uint32_t c = g - __shfl_sync(0xffffffffu, excl, L);
+            const long long b = __shfl_sync(0xffffffffu, base, L);
+            if (ELL) {
+                const uint32_t ln = __shfl_sync(0xffffffffu, len, L);
+                if (g < total) {
+                    const int4 v = ld_stream16(s.ell + b + 2 * c, pol);
+                    recv_add<R64>(rnext, v.x, v.y);
+                    if (2 * c + 1 < ln) recv_add<R64>(rnext, v.z, v.w);
+                }
+            } else {
+                const int a = __shfl_sync(0xffffffffu, amount, L);
+                if (g < total) recv_add<R64>(rnext, (int)ld_stream4(s.sdst + b + c, pol), a);
+            }
+        }
+    }
+
+    if (stats_on) {
+        stat[ST_EDGES] = (unsigned int)edges;
+        flush_stats(ctl, stat);
+    }
+    const bool bf = __syncthreads_or(t_fired);
+    const bool bc = __syncthreads_or(t_closed);
+    __shared__ long long sh_neg_idx, sh_neg_val;
+    if (threadIdx.x == 0) sh_neg_idx = 0x7fffffffffffffffll;
+    __syncthreads();
+    if (t_neg) atomicMin(&sh_neg_idx, neg_idx);
+    __syncthreads();
+    if (t_neg && sh_neg_idx == neg_idx) sh_neg_val = neg_val;
+    const bool bn = __syncthreads_or(t_neg);
+    if (threadIdx.x == 0) finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Binned push step (runs of ELL / COMPRESSED-push systems, every neuron <= 32
+// rules): the scatter of Alg. 4 / Alg. 5 without global atomics per pair.
+// L2 RED.ADD tops out near 200 G ops/s on this B200 (tools/redbench.cu), i.e.
+// ~0.9 ms for K3's 160 M deliveries, so deliveries are instead binned by
+// destination tile through shared memory and accumulated by the tile's owner
+// in the next step's kernel with shared-memory atomics.
+//
+// Destinations are cut into bin_ntiles tiles of bin_T.  One kernel per step k;
+// a CTA owns tiles and for each tile:
+//   A. receive: the tile's bin entries written during step k-1 (region
+//      bin_off[t], bin_fill[(k+1)&1][t] entries) -> 8/16/32-bit counters in
+//      shared memory;
+//   B. for 1024 destinations at a time: finish step k-1 (C += open ? recv),
+//      update delays, select step k (sv_calc), consume (row 0 of the ELL
+//      column, applied at selection like COMPRESSED);
+//   C. walk the fired neurons' columns (ELL rows 1.., 16-byte coalesced loads
+//      with an L2 evict-first hint; Optimized: the out-adjacency), and stage
+//      each delivery's entry (u16 slot when every delivery carries the same
+//      amount, else u32 slot << 15 | amount) in a per-destination-tile bucket
+//      of kBinCap entries in shared memory; full buckets spill single entries
+//      to global memory (rare), and after each 1024-destination chunk every
+//      bucket is flushed with one reservation (atomicAdd on the tile's fill
+//      counter) and coalesced stores.
+// The bins of step k are complete at the kernel boundary; kernel k+1 reads
+// them.  Each tile's region holds the most deliveries its destinations can
+// receive in one step (their in-degrees), checked on every reservation.
+
+constexpr int kBinThreads = 1024;
+constexpr int kBinCap = 64;      // staged entries per destination tile per chunk
+constexpr int kBinUnroll = 4;    // column chunks in flight per lane
+
+template <bool UNIT>
+struct BinEntry {
+    using T = uint32_t;
+};
+template <>
+struct BinEntry<true> {
+    using T = uint16_t;
+};
+
+template <int CB>
+__host__ __device__ constexpr int bin_acc_words(int T) { return (acc_words<CB>(T) + 3) & ~3; }
+
+template <bool ELL, bool WIDE, bool UNIT, int CB>
+__global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __grid_constant__ DevSys s, DevState st) {
+    using E = typename BinEntry<UNIT>::T;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int NT = s.bin_ntiles, T = s.bin_T;
+    uint32_t* acc = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* cnt = acc + bin_acc_words<CB>(T);
+    E* stage = reinterpret_cast<E*>(cnt + ((NT + 3) & ~3));
+    Ctrl* ctl = st.ctrl;
+    const volatile Ctrl* vc = ctl;
+    const int halted = vc->halted;
+    const long long k = vc->step;
+    if (halted || k >= vc->stop_at) return;
+    const bool sel = k < vc->max_steps;
+    const int record = vc->record;
+    const bool stats_on = vc->stats_on != 0;
+    const long long q = s.q;
+    const StepCtx cx{k, k - vc->trace_base, q, vc->seed, nullptr, vc->policy, record, sel, stats_on};
+    const E* __restrict__ bin_in = reinterpret_cast<const E*>((k & 1) ? st.bins[0] : st.bins[1]);
+    E* bin_out = reinterpret_cast<E*>((k & 1) ? st.bins[1] : st.bins[0]);
+    uint32_t* fill_in = (k & 1) ? st.bin_fill[0] : st.bin_fill[1];
+    uint32_t* fill_out = (k & 1) ? st.bin_fill[1] : st.bin_fill[0];
+    const uint64_t pol = evict_first_policy();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t acc_s = smem_u32(acc);
+
+    unsigned int stat[ST_COUNT];
+#pragma unroll
+    for (int i = 0; i < ST_COUNT; ++i) stat[i] = 0;
+    bool t_fired = false, t_closed = false, t_neg = false, t_over = false;
+    long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
+    unsigned long long edges = 0;
+
+    for (int i = threadIdx.x; i < NT; i += kBinThreads) cnt[i] = 0;
+    for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x) {
+        const long long d0 = tile * T;
+        const int nd = (int)min((long long)T, q - d0);
+        // ---- A. receive the deliveries of step k-1 into the tile's counters
+        for (int i = threadIdx.x; i < acc_words<CB>(T); i += kBinThreads) acc[i] = 0;
+        __syncthreads();
+        {
+            const uint32_t nin = k > 0 ? *(volatile uint32_t*)(fill_in + tile) : 0u;
+            const E* src = bin_in + __ldg(s.bin_off + tile);  // 16-byte aligned
+            constexpr int kPer = 16 / (int)sizeof(E);
+            const uint32_t nv = nin / kPer;
+            for (uint32_t v = threadIdx.x; v < nv; v += kBinThreads) {
+                const uint4 w = __ldcs(reinterpret_cast<const uint4*>(src) + v);
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    if (UNIT) {
+                        tile_acc_add_slot<CB>(acc_s, ws[x] & 0xffffu, 1u);
+                        tile_acc_add_slot<CB>(acc_s, ws[x] >> 16, 1u);
+                    } else {
+                        tile_acc_add_slot<CB>(acc_s, ws[x] >> 15, ws[x] & 0x7fffu);
+                    }
+                }
+            }
+            for (uint32_t i = nv * kPer + threadIdx.x; i < nin; i += kBinThreads) {
+                const uint32_t e = src[i];
+                if (UNIT) tile_acc_add_slot<CB>(acc_s, e, 1u);
+                else tile_acc_add_slot<CB>(acc_s, e >> 15, e & 0x7fffu);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && k > 0) fill_in[tile] = 0;  // the region is refilled in step k+1
+        // ---- B + C, 1024 destinations at a time
+        for (int c0 = 0; c0 < nd; c0 += kBinThreads) {
+            const int li = c0 + threadIdx.x;
+            const long long j = d0 + li;
+            int r = -1;
+            long long pval = 0;
+            if (li < nd) {
+                const uint32_t r0 = __ldg(s.roff + j), nr = __ldg(s.roff + j + 1) - r0;
+                const long long Cprev = st.cfg[j];
+                const int dsv = st.ds[j];
+                const bool open_prev = ds_open(dsv);
+                const int D = ds_next(dsv);
+                const bool can_sel = sel && D == 0;
+                using Raw = typename RuleRaw<WIDE>::T;
+                Raw w0{}, w1{}, w2{}, w3{};
+                if (can_sel) {
+                    if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                    if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                    if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                    if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                }
+                long long C = Cprev;
+                if (open_prev) {
+                    const uint32_t g = tile_acc_get<CB>(acc, li);
+                    C += UNIT ? (long long)g * s.bin_amount : (long long)g;
+                }
+                pval = light_commit<RECV_PULL, P_BIT, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D,
+                                                                        can_sel, stat, t_fired, t_closed, t_neg,
+                                                                        neg_idx, neg_val, r);
+            }
+            // this lane's column: chunks (ELL: 16-byte pairs of rows, row 0 =
+            // consumption, already applied; Optimized: one target per lane)
+            uint32_t nch = 0, len = 0;
+            long long base = 0;
+            if (sel && r >= 0) {
+                if (ELL) {
+                    len = __ldg(s.ell_len + r);
+                    nch = len > 1 ? (len + 1) >> 1 : 0u;
+                    base = (long long)r * s.ell_ld;
+                    edges += len > 0 ? len - 1 : 0;
+                } else if (pval > 0) {
+                    const uint32_t e0 = __ldg(s.soff + j);
+                    len = __ldg(s.soff + j + 1) - e0;
+                    nch = len;
+                    base = e0;
+                    edges += len;
+                }
+            }
+            uint32_t incl = nch;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t excl = incl - nch;
+            const int amount = (int)pval;
+            auto deliver = [&](int t, int a) {
+                const uint32_t dt = (uint32_t)__umul64hi((unsigned long long)(uint32_t)t, s.bin_magic);
+                const uint32_t slot = (uint32_t)t - dt * (uint32_t)T;
+                const E e = UNIT ? (E)slot : (E)((slot << 15) | (uint32_t)a);
+                const uint32_t pos = atomicAdd(cnt + dt, 1u);
+                if (pos < (uint32_t)kBinCap) {
+                    stage[dt * kBinCap + pos] = e;
+                } else {  // bucket full: one entry straight to the tile's region
+                    const uint32_t g = atomicAdd(fill_out + dt, 1u);
+                    const uint32_t o = __ldg(s.bin_off + dt);
+                    if (o + g < __ldg(s.bin_off + dt + 1)) bin_out[o + g] = e;
+                    else t_over = true;
+                }
+            };
+            for (uint32_t g0 = 0; g0 < total; g0 += 32 * kBinUnroll) {
+                int4 v[kBinUnroll];
+                uint32_t cc[kBinUnroll], ln[kBinUnroll];
+                int am[kBinUnroll];
+#pragma unroll
+                for (int u = 0; u < kBinUnroll; ++u) {
+                    const uint32_t g = g0 + u * 32 + lane;
+                    int L = 0;
+#pragma unroll
+                    for (int w = 16; w > 0; w >>= 1) {
+                        const uint32_t x = __shfl_sync(0xffffffffu, incl, L + w - 1);
+                        if (x <= g) L += w;
+                    }
+                    cc[u] = g - __shfl_sync(0xffffffffu, excl, L);
+                    const long long b = __shfl_sync(0xffffffffu, base, L);
+                    ln[u] = __shfl_sync(0xffffffffu, len, L);
+                    am[u] = __shfl_sync(0xffffffffu, amount, L);
+                    v[u] = make_int4(-1, 0, -1, 0);
+                    if (g < total) {
+                        if (ELL) v[u] = ld_stream16(s.ell + b + 2 * cc[u], pol);
+                        else v[u].x = (int)ld_stream4(s.sdst + b + cc[u], pol);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kBinUnroll; ++u) {
+                    if (g0 + u * 32 + lane >= total) continue;
+                    if (ELL) {
+                        if (cc[u] > 0) deliver(v[u].x, v[u].y);             // row 2c (row 0 = consumption)
+                        if (2 * cc[u] + 1 < ln[u]) deliver(v[u].z, v[u].w);  // row 2c + 1
+                    } else {
+                        deliver(v[u].x, am[u]);
+                    }
+                }
+            }
+            __syncthreads();
+            // flush every bucket: one reservation, coalesced stores
+            for (int dt = warp; dt < NT; dt += kBinThreads / 32) {
+                const uint32_t c = cnt[dt];
+                if (c == 0) continue;
+                const uint32_t n = min(c, (uint32_t)kBinCap);
+                uint32_t g = 0;
+                if (lane == 0) g = atomicAdd(fill_out + dt, n);
+                g = __shfl_sync(0xffffffffu, g, 0);
+                const uint32_t o = __ldg(s.bin_off + dt), cap = __ldg(s.bin_off + dt + 1) - o;
+                if (g + n > cap) {
+                    t_over = true;
+                } else {
+                    for (uint32_t i = lane; i < n; i += 32) bin_out[o + g + i] = stage[dt * kBinCap + i];
+                }
+                __syncwarp();
+                if (lane == 0) cnt[dt] = 0;
+            }
+            __syncthreads();
+        }
+    }
+
+    if (stats_on) {
+        stat[ST_EDGES] = (unsigned int)edges;
+        flush_stats(ctl, stat);
+    }
+    if (__syncthreads_or(t_over) && threadIdx.x == 0) atomicOr(&ctl->fault, 1);  // bin overflow (never expected)
+    const bool bf = __syncthreads_or(t_fired);
+    const bool bc = __syncthreads_or(t_closed);
+    __shared__ long long sh_neg_idx, sh_neg_val;
+    if (threadIdx.x == 0) sh_neg_idx = 0x7fffffffffffffffll;
+    __syncthreads();
+    if (t_neg) atomicMin(&sh_neg_idx, neg_idx);
+    __syncthreads();
+    if (t_neg && sh_neg_idx == neg_idx) sh_neg_val = neg_val;
+    const bool bn = __syncthreads_or(t_neg);
+    if (threadIdx.x == 0) finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0);
+}
+
 // Dense S.M (paper Alg. 3 over the fired rows only): blockIdx.x tiles 1024
 // columns (int4 per thread), blockIdx.y splits the fired-rule list.
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void __launch_bounds__(kBlock) dense_kernel(const __grid_constant__ DevSys s, DevState st) {
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
@@ -1881,6 +2368,8 @@ __global__ void __launch_bounds__(kBlock) dense_kernel(const __grid_constant__ D
     if (vc->stats_on && blockIdx.x == 0 && threadIdx.x == 0 && blockIdx.y == 0)
         atomicAdd(&ctl->stats[ST_EDGES], (unsigned long long)n * (unsigned long long)s.q);
 }
+
+#endif  // SNP_TEMPLATES_ONLY
 
 // ---------------------------------------------------------------------------
 // Phase-API helpers.
@@ -1926,6 +2415,7 @@ __global__ void prime_kernel(const __grid_constant__ DevSys s, DevState st, cons
 }
 
 // update_delays (engine.py:358-366): no source-open filter, like the reference.
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void update_delays_kernel(long long q, const int4* __restrict__ rrec,
                                      const long long* __restrict__ D,
                                      const long long* __restrict__ chosen, long long* out) {
@@ -1935,6 +2425,7 @@ __global__ void update_delays_kernel(long long q, const int4* __restrict__ rrec,
     const long long d = D[j];
     out[j] = r >= 0 ? (long long)rrec[r].z : (d > 0 ? d - 1 : 0);
 }
+#endif
 
 // Load (C, D) so that the next step kernel finalises exactly C_k = C, D_k = D
 // and then selects (sv_calc of engine.py:192-236).
@@ -1960,6 +2451,7 @@ __global__ void __launch_bounds__(256) digest_rows_kernel(const T* __restrict__ 
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out + blockIdx.y, acc);
 }
 
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void load_state_kernel(long long q, long long* cfg, int* ds, const long long* __restrict__ C,
                                   const long long* __restrict__ D) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1967,13 +2459,17 @@ __global__ void load_state_kernel(long long q, long long* cfg, int* ds, const lo
     cfg[j] = C[j];
     ds[j] = (int)(D[j] + 1);  // ds_next(D+1) == D, and not "open last step"
 }
+#endif
 
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void widen_i32_kernel(long long n, const int* __restrict__ in, long long* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = in[i];
 }
+#endif
 
 // D_k from the delay state after a halt (the last kernel ran without selection).
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void ds_to_delay_kernel(long long q, const int* __restrict__ ds, long long* out) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < q) {
@@ -1981,18 +2477,22 @@ __global__ void ds_to_delay_kernel(long long q, const int* __restrict__ ds, long
         out[j] = v < 0 ? -v - 1 : v;  // after a halt ds holds D_k directly (no firing)
     }
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // Device-side layout builders (from the CSR out-adjacency).
 
 // In-degree histogram of the transpose.
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void indeg_kernel(long long S, const uint32_t* __restrict__ dst, uint32_t* indeg) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < S;
          e += (long long)gridDim.x * blockDim.x)
         atomicAdd(indeg + dst[e], 1u);
 }
+#endif
 
 // Scatter sources into their destination lists (cursor = padded offsets).
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void transpose_fill_kernel(long long q, const uint32_t* __restrict__ soff,
                                       const uint32_t* __restrict__ sdst, uint32_t* cursor,
                                       uint32_t* isrc) {
@@ -2003,8 +2503,10 @@ __global__ void transpose_fill_kernel(long long q, const uint32_t* __restrict__ 
         isrc[pos] = (uint32_t)i;
     }
 }
+#endif
 
 // ELL columns per rule: (owner, -c) then (dst, p) for sending rules.
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void build_ell_kernel(long long m, long long ld, const uint32_t* __restrict__ owner,
                                  const int4* __restrict__ rrec, const uint32_t* __restrict__ soff,
                                  const uint32_t* __restrict__ sdst, int2* ell, uint32_t* len) {
@@ -2020,8 +2522,10 @@ __global__ void build_ell_kernel(long long m, long long ld, const uint32_t* __re
     }
     len[r] = n;
 }
+#endif
 
 // Dense rows: -c at the owner, +p at every out-neighbour (matrices.py:143-154).
+#ifndef SNP_TEMPLATES_ONLY
 __global__ void build_dense_kernel(long long m, long long ld, const uint32_t* __restrict__ owner,
                                    const int4* __restrict__ rrec, const uint32_t* __restrict__ soff,
                                    const uint32_t* __restrict__ sdst, int* dense) {
@@ -2034,5 +2538,6 @@ __global__ void build_dense_kernel(long long m, long long ld, const uint32_t* __
     if (rec.y > 0)
         for (uint32_t e = soff[o]; e < soff[o + 1]; ++e) row[sdst[e]] = rec.y;
 }
+#endif
 
 }  // namespace snp

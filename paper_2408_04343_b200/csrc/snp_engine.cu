@@ -133,6 +133,13 @@ struct snp_engine {
     DevState st{};
     StepFn step_fn = nullptr;
     StepFn lean_fn = nullptr;  // tiled: instance without recording / counters
+    StepFn fused_fn = nullptr; // push formats: one-kernel step (push_step_kernel) for runs
+    bool recv64 = false;       // fused push: 64-bit receive buffers
+    int fused_grid = 0, fused_block = 0;
+    size_t fused_smem = 0;
+    int bin_cb = 0;            // binned push: counter bits (0 = not binned)
+    bool bin_unit = false;     // binned push: u16 slot entries
+    size_t bin_smem = 0;       // binned push: dynamic shared memory
     PrimeFn prime_fn = nullptr;
     int step_grid = 0;
     int push_grid = 0;
@@ -203,13 +210,18 @@ int grid_for(long long n, int block = 256) {
 
 // Row partition (multi-GPU): this engine owns global neurons [lo, hi); the
 // edges into them come from every source, and sources are renumbered into the
-// exchange space where rank r's chunk starts at bit r * (nl + 128).
+// exchange space where rank r's chunk starts at element r * (nl + hdr): its
+// nl P elements (1, 8, 16 or 32 bits each, the same width on every rank),
+// then a 4-word header of step flags (hdr = 128 / element bits elements).
 struct ShardInput {
     int world = 1, rank = 0;
     long long q_global = 0, nl = 0, lo = 0, hi = 0;
+    int x_pbits = 0;          // agreed P element width (0: decide from this rank's rules)
+    long long x_pmax = 0;     // agreed largest produced amount over every rank
+    mutable long long hdr = 128;  // header elements, set once the P width is known
     std::vector<uint32_t> soff, sdst;  // global out-adjacency
     uint32_t xpos(uint32_t src) const {
-        return (uint32_t)((src / nl) * (nl + 128) + src % nl);
+        return (uint32_t)((src / nl) * (nl + hdr) + src % nl);
     }
 };
 
@@ -309,7 +321,11 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
     cudaFuncAttributes fa{};
-    CU(cudaFuncGetAttributes(&fa, tiled_step_kernel<P_BIT, RW_WIDE, 32, false>));
+    {
+        TiledFn probe = nullptr, probe_lean = nullptr;
+        tiled_fns<P_BIT>(RW_WIDE, 32, &probe, &probe_lean);
+        CU(cudaFuncGetAttributes(&fa, (const void*)probe));
+    }
     const long long budget = (long long)smem_optin - (long long)fa.sharedSizeBytes - 128;
     auto acc_b = [&](long long t) {
         return 4ll * (e->cbits == 8 ? acc_words<8>((int)t) : (e->cbits == 16 ? acc_words<16>((int)t) : acc_words<32>((int)t)));
@@ -743,36 +759,25 @@ int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, 
 // Build every device structure.  Host-side work is O(q + m + S) with plain
 // loops; the quadratic layouts (ELL pairs, dense rows) and the in-adjacency
 // transpose are built on the device.
-template <int PM, int RW>
-void pick_tiled_rw(snp_engine* e) {
-    switch (e->cbits) {
-        case 8:
-            e->step_fn = tiled_step_kernel<PM, RW, 8, false>;
-            e->lean_fn = tiled_step_kernel<PM, RW, 8, true>;
-            break;
-        case 16:
-            e->step_fn = tiled_step_kernel<PM, RW, 16, false>;
-            e->lean_fn = tiled_step_kernel<PM, RW, 16, true>;
-            break;
-        default:
-            e->step_fn = tiled_step_kernel<PM, RW, 32, false>;
-            e->lean_fn = tiled_step_kernel<PM, RW, 32, true>;
-    }
-}
-
 template <int PM>
 void pick_tiled(snp_engine* e) {
-    if (e->wide_rules) pick_tiled_rw<PM, RW_WIDE>(e);
-    else if (e->tiny_rules) pick_tiled_rw<PM, RW_TINY>(e);
-    else pick_tiled_rw<PM, RW_COMPACT>(e);
+    const int rw = e->wide_rules ? RW_WIDE : (e->tiny_rules ? RW_TINY : RW_COMPACT);
+    tiled_fns<PM>(rw, e->cbits, &e->step_fn, &e->lean_fn);
     e->prime_fn = prime_kernel<RECV_PULL, PM, true, false>;
 }
 
 // The step kernel instance for the current run parameters: the lean tiled
 // instance when nothing is recorded or counted.
 StepFn run_fn(const snp_engine* e) {
+    if (e->fused_fn) return e->fused_fn;
     if (e->lean_fn && e->hctrl.record == 0 && !e->hctrl.stats_on) return e->lean_fn;
     return e->step_fn;
+}
+
+// The step kernel of a run (the one-kernel push step when the engine has one).
+void launch_main(snp_engine* e) {
+    if (e->fused_fn) e->fused_fn<<<e->fused_grid, e->fused_block, e->fused_smem, e->stream>>>(e->sys, e->st);
+    else run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
 }
 
 // SNPB200_TIMING=1: per-phase host timings of engine creation on stderr
@@ -852,6 +857,23 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             if (pfirst < 0) pfirst = x.y;
             else if (x.y != pfirst) pcommon = false;
         }
+    }
+
+    if (sh && sh->x_pbits) {
+        // row partition: every rank must use the same exchange width (and, for
+        // P bits, the same common amount), agreed over all ranks by the caller
+        const int xb = sh->x_pbits;
+        if (xb != 1 && xb != 8 && xb != 16 && xb != 32)
+            return fail(SNP_ERR_BAD_ARG, "x_pbits must be 1, 8, 16 or 32, got %d", xb);
+        if (pmax > sh->x_pmax || (xb == 1 && pfirst >= 0 && (!pcommon || pfirst != sh->x_pmax)))
+            return fail(SNP_ERR_BAD_ARG, "this rank's produced amounts disagree with the agreed exchange (x_pbits=%d, "
+                        "x_pmax=%lld)", xb, sh->x_pmax);
+        const long long cap = xb == 1 ? (1ll << 31) : (xb == 32 ? (1ll << 32) : (1ll << xb));
+        if (sh->x_pmax < 1 || sh->x_pmax >= cap)
+            return fail(SNP_ERR_BAD_ARG, "x_pmax=%lld does not fit x_pbits=%d", sh->x_pmax, xb);
+        pcommon = xb == 1;
+        pfirst = sh->x_pmax;
+        pmax = sh->x_pmax;
     }
 
     tm.mark("rule vector");
@@ -975,13 +997,14 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     if (pcommon) {
         e->p_mode = P_BIT;
         e->p_common = pfirst > 0 ? pfirst : 1;
-    } else if (pmax <= 255) {
+    } else if (pmax <= 255 && !(sh && sh->x_pbits > 8)) {
         e->p_mode = P_U8;
-    } else if (pmax <= 65535) {
+    } else if (pmax <= 65535 && !(sh && sh->x_pbits > 16)) {
         e->p_mode = P_U16;
     } else {
         e->p_mode = P_U32;
     }
+    if (sh) sh->hdr = 128 / (e->p_mode == P_BIT ? 1 : (e->p_mode == P_U8 ? 8 : (e->p_mode == P_U16 ? 16 : 32)));
 
     CU(cudaSetDevice(e->device));
     CU(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
@@ -1099,8 +1122,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         const bool many_in = e->kind == RECV_PULL && !e->tiled && ((indeg[i] + 3u) & ~3u) > kLightIn;
         if (many_rules || many_in) heavy.push_back((uint32_t)i);
     }
-    if (sh && !(e->tiled && e->p_mode == P_BIT))
-        return fail(SNP_ERR_BAD_ARG, "row partition needs COMPRESSED/tiled and one common produced amount (P bits)");
+    if (sh && !e->tiled) return fail(SNP_ERR_BAD_ARG, "row partition needs COMPRESSED/tiled");
     tm.mark("in-adjacency / heavy");
     if (e->tiled) TRY(build_tiles(e, d, soff, sdst, roff, heavy, sh, d_soff, d_sdst));
     uint32_t* d_heavy;
@@ -1196,26 +1218,154 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     }
 
     tm.mark("tiled layout + formats");
+    // --- one-kernel push step for runs (ELL / COMPRESSED-push, every neuron
+    // <= 32 rules): the binned kernel (ell_bin_step_kernel) when deliveries
+    // fit its entries, else the L2-atomic one (push_step_kernel).
+    // SNPB200_PUSH=atomic forces the latter, =unfused the 3-kernel path.
+    const char* push_env = getenv("SNPB200_PUSH");
+    if (e->kind == RECV_ARRAY && e->format != SNP_FMT_SPARSE && s.n_heavy == 0 && q > 0 &&
+        !(push_env && !strcmp(push_env, "unfused"))) {
+        // per destination: deliveries it can receive in one step (each source
+        // fires at most one rule) and their largest amount
+        std::vector<uint32_t> ind(q, 0);
+        long long amax = 0, amin = 0, cmax = 0;
+        bool amount_common = true;
+        if (have_adj) {
+            if (!sdst.empty()) {
+                uint32_t* d_in;
+                CU(cudaMalloc(&d_in, (size_t)q * 4));
+                CU(cudaMemset(d_in, 0, (size_t)q * 4));
+                indeg_kernel<<<std::min(grid_for((long long)sdst.size()), 148 * 64), 256>>>((long long)sdst.size(), d_sdst, d_in);
+                cudaError_t err = cudaGetLastError();
+                if (err == cudaSuccess) err = cudaMemcpy(ind.data(), d_in, (size_t)q * 4, cudaMemcpyDeviceToHost);
+                cudaFree(d_in);
+                CU(err);
+            }
+            amax = pmax;
+            amin = pfirst;
+            amount_common = pcommon;
+            if (e->format == SNP_FMT_ELL)
+                for (long long r = 0; r < m; ++r) cmax = std::max<long long>(cmax, rrec[r].x);
+        } else {
+            // ELL given as the reference matrix: count every delivery pair (an
+            // upper bound: rules of one neuron never fire together)
+            for (long long r = 0; r < m; ++r)
+                for (uint32_t n = 1; n < ell_len_host[r]; ++n) {
+                    const int2 pr = ell_host[r * ell_ld + n];
+                    ind[pr.x] += 1;
+                    const long long a = std::abs((long long)pr.y);
+                    if (amin == 0) amin = a;
+                    amount_common = amount_common && a == amin && pr.y > 0;
+                    amax = std::max(amax, a);
+                }
+            for (long long r = 0; r < m; ++r)
+                if (ell_len_host[r]) cmax = std::max<long long>(cmax, std::abs((long long)ell_host[r * ell_ld].y));
+        }
+        uint32_t mx = 0;
+        for (uint32_t x : ind) mx = std::max(mx, x);
+        // binned: u16 slots (common amount) or u32 slot << 15 | amount (< 2^15)
+        const bool unit = amount_common && amin > 0;
+        bool bins_ok = (unit || (amin >= 0 && amax < (1 << 15))) && !(push_env && !strcmp(push_env, "atomic"));
+        if (ell_from_matrix)  // the binned kernel consumes at selection: row 0 must be (owner, -consumed)
+            for (long long r = 0; r < m && bins_ok; ++r)
+                bins_ok = ell_len_host[r] >= 1 && ell_host[r * ell_ld].x == (int)owner[r] &&
+                          ell_host[r * ell_ld].y == -rrec[r].x;
+        const long long recv_worst = (long long)mx * (unit ? 1 : std::max<long long>(1, amax));
+        int n_sm = 148;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, e->device);
+        int smem_optin = 0;
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
+        bool binned = false;
+        if (bins_ok && recv_worst < (1ll << 32)) {
+            const int cb = recv_worst < 256 ? 8 : (recv_worst < 65536 ? 16 : 32);
+            const long long tmax = unit ? 65536 : 131072;
+            long long per_sm = 2;
+            if (const char* env = getenv("SNPB200_BIN_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
+            long long T = std::min<long long>(tmax, (ceil_div(q, per_sm * n_sm) + 31) / 32 * 32);
+            const long long nt = ceil_div(q, T);
+            const size_t esz = unit ? 2 : 4;
+            const size_t acc_b = 4 * (size_t)(cb == 8 ? bin_acc_words<8>((int)T)
+                                                      : (cb == 16 ? bin_acc_words<16>((int)T) : bin_acc_words<32>((int)T)));
+            const size_t smem = acc_b + 4 * (size_t)((nt + 3) & ~3ll) + (size_t)nt * kBinCap * esz;
+            if ((long long)smem + 2048 <= smem_optin) {
+                binned = true;
+                // bin regions: the in-degree of the tile's destinations, 16-byte aligned
+                std::vector<uint32_t> boff(nt + 1, 0);
+                unsigned long long tot = 0;
+                for (long long t = 0; t < nt; ++t) {
+                    unsigned long long c = 0;
+                    for (long long jj = t * T; jj < std::min<long long>(q, (t + 1) * T); ++jj) c += ind[jj];
+                    boff[t] = (uint32_t)tot;
+                    tot += (c + 7) & ~7ull;
+                    if (tot >= (1ull << 32) - 8) return fail(SNP_ERR_CAPACITY, "push bins exceed 2^32 entries");
+                }
+                boff[nt] = (uint32_t)tot;
+                uint32_t* d_boff;
+                TRY(upload(e, &d_boff, boff));
+                for (int i = 0; i < 2; ++i) {
+                    uint4* bb;
+                    TRY(e->alloc(&bb, (long long)(tot * esz + 15) / 16 + 1));
+                    st.bins[i] = bb;
+                    TRY(e->alloc(&st.bin_fill[i], nt));
+                }
+                s.bin_T = (int)T;
+                s.bin_ntiles = (int)nt;
+                s.bin_magic = (~0ull / (unsigned long long)T) + 1ull;
+                s.bin_amount = unit ? (int)amin : 1;
+                s.bin_off = d_boff;
+                e->bin_cb = cb;
+                e->bin_unit = unit;
+                e->bin_smem = smem;
+                const bool ell = e->format == SNP_FMT_ELL, w = e->wide_rules;
+#define SNP_BIN_PICK(E_, W_, U_)                                                                    \
+    (cb == 8 ? ell_bin_step_kernel<E_, W_, U_, 8> : (cb == 16 ? ell_bin_step_kernel<E_, W_, U_, 16>  \
+                                                              : ell_bin_step_kernel<E_, W_, U_, 32>))
+                if (ell) e->fused_fn = w ? (unit ? SNP_BIN_PICK(true, true, true) : SNP_BIN_PICK(true, true, false))
+                                         : (unit ? SNP_BIN_PICK(true, false, true) : SNP_BIN_PICK(true, false, false));
+                else e->fused_fn = w ? (unit ? SNP_BIN_PICK(false, true, true) : SNP_BIN_PICK(false, true, false))
+                                     : (unit ? SNP_BIN_PICK(false, false, true) : SNP_BIN_PICK(false, false, false));
+#undef SNP_BIN_PICK
+                CU(cudaFuncSetAttribute(e->fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            }
+        }
+        if (!binned) {
+            // L2 atomics into int32 receive buffers unless some neuron could
+            // receive 2^31 or more (in absolute value) in one step
+            const long long worst = (long long)mx * std::max<long long>(1, amax) + cmax;
+            e->recv64 = worst >= (1ll << 31);
+            const bool ell = e->format == SNP_FMT_ELL, w = e->wide_rules, r64 = e->recv64;
+            e->fused_fn = ell ? (w ? (r64 ? push_step_kernel<true, true, true> : push_step_kernel<true, true, false>)
+                                   : (r64 ? push_step_kernel<true, false, true> : push_step_kernel<true, false, false>))
+                              : (w ? (r64 ? push_step_kernel<false, true, true> : push_step_kernel<false, true, false>)
+                                   : (r64 ? push_step_kernel<false, false, true> : push_step_kernel<false, false, false>));
+            for (int i = 0; i < 2; ++i) {
+                long long* bb;
+                TRY(e->alloc(&bb, r64 ? q : (q + 1) / 2));
+                st.rbuf[i] = bb;
+            }
+        }
+    }
+
     // --- run state
     TRY(e->alloc(&st.cfg, q + 8));  // +8: 16-byte bulk-copy tails
     TRY(e->alloc(&st.ds, q + 8));
     TRY(e->alloc(&st.chosen, q));
     if (sh) {
-        s.x_stride = sh->nl / 32 + 4;
+        s.x_stride = sh->nl * 128 / sh->hdr / 32 + 4;  // P elements, then 4 header words
         s.world = sh->world;
         s.rank = sh->rank;
         s.gbase = sh->lo;
-        s.xbase = (long long)sh->rank * s.x_stride * 32;
+        s.xbase = (long long)sh->rank * (sh->nl + sh->hdr);  // in P elements
         // identical on every rank (peers address each other's flags at
         // 3 * p_words): the two-pass tail covers any window size <= 2^16
         e->p_words = s.x_stride * sh->world + 8 + (s.tp ? (1ll << (16 - 5)) : 0);
     }
     if (e->kind == RECV_PULL) {
         long long words;
-        switch (e->p_mode) {
+        switch (sh ? -1 : e->p_mode) {
+            case -1: words = e->p_words; break;  // row partition: the exchange space
             case P_BIT:  // +8: bulk-copy tails; two-pass: whole source windows
-                words = sh ? e->p_words
-                           : std::max<long long>(ceil_div(q + 1, 32) + 8, s.tp ? s.tp_nw * (1ll << (s.tp_wlog - 5)) + 8 : 0);
+                words = std::max<long long>(ceil_div(q + 1, 32) + 8, s.tp ? s.tp_nw * (1ll << (s.tp_wlog - 5)) + 8 : 0);
                 break;
             case P_U8: words = ceil_div(q + 1, 4) + 1; break;
             case P_U16: words = ceil_div(q + 1, 2) + 1; break;
@@ -1289,6 +1439,19 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         e->step_grid = s.light_ctas + s.heavy_ctas;
         e->resident_ctas = resident;
     }
+    if (e->fused_fn && e->bin_cb) {
+        int per = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, e->fused_fn, kBinThreads, e->bin_smem));
+        e->fused_grid = (int)std::min<long long>(s.bin_ntiles, (long long)std::max(1, per) * n_sm);
+        e->fused_block = kBinThreads;
+        e->fused_smem = e->bin_smem;
+    } else if (e->fused_fn) {
+        int per = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, e->fused_fn, kBlock, 0));
+        e->fused_grid = (int)std::min<long long>(s.light_tiles, (long long)std::max(1, per) * n_sm);
+        e->fused_block = kBlock;
+        e->fused_smem = 0;
+    }
     CU(cudaDeviceSynchronize());
     return SNP_OK;
 }
@@ -1301,24 +1464,27 @@ int launch_pass1(snp_engine* e) {
     return 1;
 }
 
+// The scatter kernels that follow an unfused push-format step kernel.
+int launch_push_tail(snp_engine* e, long long* row_visits = nullptr) {
+    if (e->kind != RECV_ARRAY || e->fused_fn) return 0;
+    if (e->format == SNP_FMT_SPARSE) {
+        dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+        return 1;
+    }
+    if (e->format == SNP_FMT_ELL) {
+        push_kernel<true><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, row_visits);
+        push_heavy_kernel<true><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+    } else {
+        push_kernel<false><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, row_visits);
+        push_heavy_kernel<false><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
+    }
+    return 2;
+}
+
 int launch_step(snp_engine* e, long long* row_visits = nullptr) {
     int n = 1 + launch_pass1(e);
-    run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
-    if (e->kind == RECV_ARRAY) {
-        if (e->format == SNP_FMT_SPARSE) {
-            dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
-            n += 1;
-        } else if (e->format == SNP_FMT_ELL) {
-            push_kernel<true><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, row_visits);
-            push_heavy_kernel<true><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
-            n += 2;
-        } else {
-            push_kernel<false><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, row_visits);
-            push_heavy_kernel<false><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
-            n += 2;
-        }
-    }
-    return n;
+    launch_main(e);
+    return n + launch_push_tail(e, row_visits);
 }
 
 int push_ctrl(snp_engine* e) {
@@ -1329,6 +1495,8 @@ int push_ctrl(snp_engine* e) {
 int pull_ctrl(snp_engine* e) {
     CU(cudaMemcpyAsync(&e->hctrl, e->st.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
+    if (e->hctrl.fault)
+        return fail(SNP_ERR_CUDA, "internal error: a binned-push bin region overflowed at step %lld", e->hctrl.step);
     return SNP_OK;
 }
 
@@ -1340,8 +1508,9 @@ int reset_state(snp_engine* e) {
         // OR-accumulated into zeroed buffers
         for (int i = 0; i < 3; ++i) {
             size_t bytes;
-            switch (e->p_mode) {
-                case P_BIT: bytes = (e->p_words ? e->p_words : e->p_bit_words) * 4; break;
+            switch (e->p_words ? -1 : e->p_mode) {
+                case -1: bytes = e->p_words * 4; break;  // row partition: the exchange space
+                case P_BIT: bytes = e->p_bit_words * 4; break;
                 case P_U8: bytes = (ceil_div(q + 1, 4) + 1) * 4; break;
                 case P_U16: bytes = (ceil_div(q + 1, 2) + 1) * 4; break;
                 default: bytes = (q + 2) * 4; break;
@@ -1350,6 +1519,13 @@ int reset_state(snp_engine* e) {
         }
     } else {
         CU(cudaMemsetAsync(st.recv, 0, std::max<long long>(1, q) * 8, e->stream));
+        if (e->fused_fn && e->bin_cb) {
+            for (int i = 0; i < 2; ++i)
+                CU(cudaMemsetAsync(st.bin_fill[i], 0, (size_t)std::max(1, e->sys.bin_ntiles) * 4, e->stream));
+        } else if (e->fused_fn) {
+            for (int i = 0; i < 2; ++i)
+                CU(cudaMemsetAsync(st.rbuf[i], 0, std::max<long long>(1, q) * (e->recv64 ? 8 : 4), e->stream));
+        }
     }
     CU(cudaMemsetAsync(st.ds, 0, std::max<long long>(1, q) * 4, e->stream));
     CU(cudaMemsetAsync(st.chosen, 0xff, std::max<long long>(1, q) * 4, e->stream));
@@ -1399,6 +1575,7 @@ int ensure_graph(snp_engine* e, long long iters) {
 
 int kernels_per_step(const snp_engine* e) {
     if (e->kind == RECV_PULL) return e->sys.tp ? 2 : 1;
+    if (e->fused_fn) return 1;
     return e->format == SNP_FMT_SPARSE ? 2 : 3;
 }
 
@@ -1465,6 +1642,8 @@ int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
         sh.hi = std::min<long long>(q, sh.lo + sh.nl);
         TRY(check_csr_offsets(desc->adj_offsets, q));
         const long long S = q > 0 ? desc->adj_offsets[q] : 0;
+        sh.x_pbits = desc->x_pbits;
+        sh.x_pmax = desc->x_pmax;
         if (S >= (1ll << 32) - 1 || (long long)desc->world * (sh.nl + 128) >= (1ll << 32))
             return fail(SNP_ERR_CAPACITY, "row partition exceeds 32-bit exchange positions");
         sh.soff.resize(q + 1);
@@ -1518,6 +1697,10 @@ int snp_engine_get_info(const snp_engine* e, snp_engine_info* info) {
     info->ring_stages = e->tiled ? e->sys.ring : 0;
     info->counter_bits = e->tiled ? e->cbits : 0;
     info->stage_bytes = e->tiled ? (int64_t)kStageBytes : 0;
+    info->push_kernel = e->kind != RECV_ARRAY || e->format == SNP_FMT_SPARSE
+                            ? SNP_PUSH_NONE
+                            : (!e->fused_fn ? SNP_PUSH_UNFUSED : (e->bin_cb ? SNP_PUSH_BINNED : SNP_PUSH_ATOMIC));
+    info->push_tiles = e->bin_cb ? e->sys.bin_ntiles : 0;
     return SNP_OK;
 }
 
@@ -1700,24 +1883,11 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
         for (long long i = 0; i < steps; ++i) {
             launches += launch_pass1(e);
             CU(cudaEventRecord(ev[2 * i], e->stream));
-            run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
+            launch_main(e);
             CU(cudaEventRecord(ev[2 * i + 1], e->stream));
             launches += 1;
-            if (e->kind == RECV_ARRAY) {
-                // push kernels of the same step, launched after the timed one
-                if (e->format == SNP_FMT_SPARSE) {
-                    dense_kernel<<<e->dense_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
-                    launches += 1;
-                } else if (e->format == SNP_FMT_ELL) {
-                    push_kernel<true><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, nullptr);
-                    push_heavy_kernel<true><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
-                    launches += 2;
-                } else {
-                    push_kernel<false><<<e->push_grid, kBlock, 0, e->stream>>>(e->sys, e->st, nullptr);
-                    push_heavy_kernel<false><<<e->heavy_push_grid, kBlock, 0, e->stream>>>(e->sys, e->st);
-                    launches += 2;
-                }
-            }
+            // push kernels of the same step (unfused push formats), launched after the timed one
+            launches += launch_push_tail(e);
         }
         CU(cudaGetLastError());
         CU(cudaEventRecord(e->ev1, e->stream));

@@ -174,7 +174,7 @@ class DeviceEngine:
                  initial: np.ndarray | None = None, *, adj: tuple[np.ndarray, np.ndarray] | None = None,
                  syn: SynapseMatrix | None = None, ell: EllMatrix | None = None,
                  sparse: SparseMatrix | None = None, variant: str = "auto", device: int = 0,
-                 world: int = 1, rank: int = 0):
+                 world: int = 1, rank: int = 0, x_pbits: int = 0, x_pmax: int = 0):
         if fmt not in _FMT_CODES:
             raise ValueError(f"no device backend for format {fmt!r}")
         if variant not in _VARIANTS:
@@ -215,6 +215,7 @@ class DeviceEngine:
             d.sparse_data = nat.i64p(keep["sparse"])
         d.device = device
         d.world, d.rank = int(world), int(rank)
+        d.x_pbits, d.x_pmax = int(x_pbits), int(x_pmax)
         handle = nat.ctypes.c_void_p()
         rc = lib.snp_engine_create(nat.ctypes.byref(d), nat.ctypes.byref(handle))
         if rc == nat.SNP_ERR_BAD_ARG:
@@ -576,7 +577,8 @@ def _content_key(*arrays) -> str:
     for x in arrays:
         x = np.ascontiguousarray(x)
         h.update(repr((x.shape, x.dtype.str)).encode())
-        h.update(memoryview(x).cast("B"))
+        if x.size:
+            h.update(memoryview(x).cast("B"))
     return h.hexdigest()
 
 

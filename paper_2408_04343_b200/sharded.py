@@ -10,9 +10,13 @@ P_k and flags visible everywhere before step k+1, whose kernel takes the
 halting decision for step k from the gathered flags -- identically on every
 rank, with no host round trip.
 
-Exchange space: rank r's chunk starts at bit r * (nl + 128); its first nl bits
-are its neurons' P bits, the last 4 words its flags.  Sources in the tiled
-in-edge segments are renumbered into this space when the engine is built.
+Exchange space: P is one element per neuron -- a bit when every sending rule
+of the whole system produces the same amount, else u8 / u16 / u32 by the
+largest produced amount (``exchange_width``; every rank must agree, so the
+caller passes the system-wide range).  Rank r's chunk starts at element
+r * (nl + hdr); its first nl elements are its neurons' P, the last 4 words
+(hdr = 128 / element bits elements) its flags.  Sources in the tiled in-edge
+segments are renumbered into this space when the engine is built.
 
 Selection hashes on the global neuron id, so a sharded run is bit-identical
 to the single-engine run (tests/test_sharded.py).
@@ -39,28 +43,64 @@ class ShardLayout:
     q: int
     world: int
     nl: int                 # neurons per rank (multiple of 128)
+    pbits: int = 1          # exchange element width (1, 8, 16, 32)
 
     def bounds(self, rank: int) -> tuple[int, int]:
         lo = min(self.q, rank * self.nl)
         return lo, min(self.q, lo + self.nl)
 
     @property
+    def hdr(self) -> int:
+        """Header elements of a rank chunk (4 words)."""
+        return HDR_BITS // self.pbits
+
+    @property
     def chunk_words(self) -> int:
-        return self.nl // 32 + HDR_BITS // 32
+        return self.nl * self.pbits // 32 + HDR_BITS // 32
 
     def xpos(self, src: np.ndarray) -> np.ndarray:
-        """Exchange-space bit position of global source ids."""
+        """Exchange-space element position of global source ids."""
         src = np.asarray(src, dtype=np.int64)
-        return (src // self.nl) * (self.nl + HDR_BITS) + src % self.nl
+        return (src // self.nl) * (self.nl + self.hdr) + src % self.nl
 
     def header_word(self, rank: int) -> int:
         return rank * self.chunk_words + self.chunk_words - 4
 
 
-def shard_layout(q: int, world: int) -> ShardLayout:
+def shard_layout(q: int, world: int, pbits: int = 1) -> ShardLayout:
     """The partition rule of snp_engine_create (include/snpb200.h)."""
     per = -(-max(q, 1) // world)
-    return ShardLayout(q, world, -(-per // 128) * 128)
+    return ShardLayout(q, world, -(-per // 128) * 128, pbits)
+
+
+def p_range(rules: RuleVector) -> tuple[int, int]:
+    """(smallest, largest) produced amount over the sending rules; (0, 0)
+    when no rule sends."""
+    p = np.asarray(rules.produced)
+    p = p[p > 0]
+    return (int(p.min()), int(p.max())) if p.size else (0, 0)
+
+
+def exchange_width(pmin: int, pmax: int) -> tuple[int, int]:
+    """(x_pbits, x_pmax) of the exchange for a system whose sending rules
+    produce amounts in [pmin, pmax]: one bit when they are all equal, else the
+    narrowest of u8 / u16 / u32 that holds pmax (the engine's P modes)."""
+    if pmax <= 0 or pmin == pmax:
+        return 1, max(1, pmax)
+    return (8 if pmax <= 255 else 16 if pmax <= 65535 else 32), pmax
+
+
+def global_p_range(rules: RuleVector, group=None) -> tuple[int, int]:
+    """p_range over every rank's rules (torch.distributed all-reduce)."""
+    import torch
+    import torch.distributed as dist
+    lo, hi = p_range(rules)
+    backend = dist.get_backend(group)
+    dev = "cuda" if backend == "nccl" else "cpu"
+    t = torch.tensor([-(lo if lo > 0 else 1 << 62), hi], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    lo = -int(t[0].item())
+    return (0 if lo == 1 << 62 else lo), int(t[1].item())
 
 
 def decide_halt(flags: np.ndarray, last: bool = False) -> HaltReason | str | None:
@@ -109,15 +149,19 @@ class ShardedEngine:
     """
 
     def __init__(self, local: SystemArrays, q: int, rank: int, world: int, device: int = 0,
-                 variant: str = "tiled"):
-        self.layout = shard_layout(q, world)
+                 variant: str = "tiled", p_span: tuple[int, int] | None = None):
+        # p_span: the system-wide (pmin, pmax) of the produced amounts (see
+        # global_p_range); every rank must pass the same one.  Default: this
+        # rank's own rules (only safe when they span the whole system's range)
+        pbits, pmax = exchange_width(*(p_span if p_span is not None else p_range(local.rules)))
+        self.layout = shard_layout(q, world, pbits)
         self.rank, self.world = rank, world
         self.lo, self.hi = self.layout.bounds(rank)
         if local.neuron_count != self.hi - self.lo:
             raise ValueError(f"rank {rank} owns {self.hi - self.lo} neurons, got {local.neuron_count}")
         self.engine = DeviceEngine(Format.COMPRESSED, q, local.rules, local.rule_map.offsets, local.initial,
                                    adj=(local.adj_offsets, local.adj_targets), variant=variant,
-                                   device=device, world=world, rank=rank)
+                                   device=device, world=world, rank=rank, x_pbits=pbits, x_pmax=pmax)
         self.x = self.engine.exchange_info()
         self._views = None
 
@@ -281,8 +325,10 @@ def synth_v1_rows_numpy(q: int, lo: int, hi: int, seed: int = SYNTH_SEED, with_d
 # -- bench entry (torchrun, N > 1) ------------------------------------------------------
 
 def bench_sharded(args, rank: int, world: int) -> None:
-    """Weak scaling: q = world x 10^7, each rank owns 10^7 rows; value is
-    whole-job 10^7-neuron-steps/s (= world x system steps/s).
+    """Weak scaling (default): q = world x 10^7, each rank owns 10^7 rows;
+    value is whole-job 10^7-neuron-steps/s (= world x system steps/s).
+    Strong scaling (``--workload k5``): K5's q = 10^8 split over the ranks;
+    value is system steps/s of the 10^8-neuron system.
 
     Exchange: peer exchange (step kernels store P chunks straight into the
     peers' slots over NVLink, no per-step collective) when every GPU pair can
@@ -309,13 +355,15 @@ def bench_sharded(args, rank: int, world: int) -> None:
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     cdev = "cpu" if same_dev else "cuda"  # device of the collectives' tensors
-    q = args.q * world
+    strong = args.workload == "k5"
+    q = 10 * args.q if strong else args.q * world
     layout = shard_layout(q, world)
     lo, hi = layout.bounds(rank)
     t0 = time.perf_counter()
     local = synth_v1_rows(q, lo, hi, with_delays=(args.workload == "k4"))
     gen_s = time.perf_counter() - t0
-    sh = ShardedEngine(local, q, rank, world, device=dev)
+    span = global_p_range(local.rules)  # every rank agrees on the exchange width
+    sh = ShardedEngine(local, q, rank, world, device=dev, p_span=span)
     ndev = torch.cuda.device_count()
     use_p2p = same_dev or (os.environ.get("SNPB200_EXCHANGE", "p2p") != "nccl" and
                            peer_access_ok(list(range(min(ndev, world)))))
@@ -346,7 +394,7 @@ def bench_sharded(args, rank: int, world: int) -> None:
         if not flag.item():
             use_p2p = False
             if sh.p2p:
-                sh = ShardedEngine(local, q, rank, world, device=dev)
+                sh = ShardedEngine(local, q, rank, world, device=dev, p_span=span)
                 sh.engine.set_stream(stream.cuda_stream)
         dist.barrier()
     ex = None if use_p2p else torch_allgather_exchange(sh)
@@ -410,11 +458,13 @@ def bench_sharded(args, rank: int, world: int) -> None:
         achieved = alg / (ms_step / 1000.0) / 1e9
         xbytes = int(sh.x.slot_bytes) - int(sh.x.chunk_bytes)
         line = {
-            "metric": "SNP steps/sec at 10^7 neurons", "value": world * 1000.0 / ms_step, "unit": "steps/s",
+            "metric": "SNP steps/sec at 10^8 neurons" if strong else "SNP steps/sec at 10^7 neurons",
+            "value": (1.0 if strong else world) * 1000.0 / ms_step, "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic (synth-v1 rows per rank)",
-            "config": {"workload": f"synth-v1 q={q} ({world} x {args.q} rows), row-partitioned",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic (synth-v1 rows per rank)",
+            "config": {"workload": (f"synth-v1 q={q} (K5) split over {world} ranks" if strong else
+                                    f"synth-v1 q={q} ({world} x {args.q} rows)") + ", row-partitioned",
                        "exchange": "p2p (NVLink stores from the step kernel)" if use_p2p else "nccl all-gather",
                        "format": "compressed", "variant": "tiled", "policy": "first",
                        "parallelism": f"rows/{world}", "exchange_bytes_per_step": int(sh.x.slot_bytes),
@@ -422,7 +472,7 @@ def bench_sharded(args, rank: int, world: int) -> None:
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "per": "GPU (rank 0's rows), whole step incl. exchange wait",
                          "nvlink_GBps_in": xbytes / (ms_step / 1000.0) / 1e9},
-            "e2e": {"value": world * e2e_n / e2e_s.item(), "unit": "steps/s",
+            "e2e": {"value": (1 if strong else world) * e2e_n / e2e_s.item(), "unit": "steps/s",
                     "h2d_bytes_per_step": 8 * q, "d2h_bytes_per_step": 8 * q,
                     "path": "ShardedEngine begin(host config) + 1 step + read_state, every rank"},
             "system_steps_per_s": 1000.0 / ms_step, "gpu_launches": args.steps, "halt": int(res.halt),

@@ -143,3 +143,22 @@ def pytest_collection_modifyitems(config, items):
     if dropped:
         config.hook.pytest_deselected(items=dropped)
         items[:] = keep
+
+
+def multi_amount_system(q: int, pmax: int, seed: int | None = None):
+    """synth-v1 with delays whose sending rules produce random amounts in
+    [1, pmax] (consumption and thresholds raised to stay consistent), so P is
+    u8 / u16 / u32 per neuron instead of bits."""
+    import paper_2408_04343_b200 as snp
+    base = snp.synth_v1(q, with_delays=True)
+    r = base.rules
+    rng = np.random.default_rng(pmax if seed is None else seed)
+    firing = r.produced > 0
+    amount = rng.integers(1, pmax + 1, size=len(r.produced))
+    produced = np.where(firing, amount, 0)
+    consumed = np.where(firing, np.maximum(r.consumed, produced), r.consumed)
+    threshold = np.where(firing & ~r.is_exact, np.maximum(r.threshold, consumed), r.threshold)
+    threshold = np.where(firing & r.is_exact, consumed, threshold)
+    rules = snp.RuleVector(threshold, r.is_exact, consumed, produced, r.delay, r.neuron)
+    initial = base.initial + rng.integers(0, 3 * pmax, size=base.neuron_count)
+    return snp.SystemArrays(initial, rules, base.rule_map, base.adj_offsets, base.adj_targets)

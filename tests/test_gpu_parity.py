@@ -121,6 +121,47 @@ def test_sort_large_halts_sorted(n, fmts):
     assert trace_digest(mine.configs, mine.delays, mine.spiking) == trace_digest(tr.configs, tr.delays, tr.spiking)
 
 
+@pytest.mark.parametrize("variant", ["tiled", "pull"])
+@pytest.mark.parametrize("policy", ["first", "seeded"])
+def test_k2_sort4096_to_halt(variant, policy):
+    """K2 (BASELINE.json configs[1]): the worst-case sorter n=4096 (values
+    n..1) runs n+1 = 4097 steps to NO_APPLICABLE_RULES and decodes 1..n
+    (test_acceptance.py:170-183); the first 50 FULL trace rows equal the C
+    oracle's (oracle.py:21-101)."""
+    n = 4096
+    a = snp.sort_arrays(snp.SortInstance(n))
+    sel, pol, seed = ((snp.FirstApplicable(), 0, 0) if policy == "first"
+                      else (snp.SeededRandom(240804343), 1, 240804343))
+    prep = snp.prepare(a, snp.Format.COMPRESSED, variant=variant)
+    res = snp.run_final(prep, snp.SimOptions(max_steps=n + 10, selection=sel))
+    assert res.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
+    assert res.steps == n + 1
+    assert res.config[2 * n:].tolist() == list(range(1, n + 1))
+    ref, _, _ = coracle.run(OracleSystem.from_arrays(a), 50, pol, seed, trace_rows=51)
+    mine = snp.simulate_prepared(prep, snp.SimOptions(max_steps=50, selection=sel, record=snp.RecordLevel.FULL))
+    assert trace_digest(mine.configs, mine.delays, mine.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
+
+
+@pytest.mark.parametrize("fmt", [snp.Format.ELL, snp.Format.SPARSE], ids=["ell", "sparse"])
+def test_sort2048_ell_sparse_to_halt(fmt):
+    """ELL (69 GB of pairs) and the dense matrix (103 GB) at sort n=2048:
+    run to halt, decode, and match the oracle's first 30 FULL rows."""
+    n = 2048
+    rng = np.random.default_rng(7)
+    values = tuple(int(v) for v in rng.choice(np.arange(1, 4 * n), size=n, replace=False))
+    a = snp.sort_arrays(snp.SortInstance(n, values))
+    prep = snp.prepare(a, fmt)
+    res = snp.run_final(prep, snp.SimOptions(max_steps=5 * n))
+    assert res.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
+    assert res.config[2 * n:].tolist() == sorted(values)
+    ref, want_c, _ = coracle.run(OracleSystem.from_arrays(a), 5 * n, 0, 0, trace_rows=31)
+    assert res.steps == ref.n_steps
+    np.testing.assert_array_equal(res.config, want_c)
+    mine = snp.simulate_prepared(prep, snp.SimOptions(max_steps=30, record=snp.RecordLevel.FULL))
+    assert trace_digest(mine.configs, mine.delays, mine.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
+    del prep
+
+
 def test_subset_sum_accepting_paths():
     t = golden_npz("traces.npz")
     prep = snp.prepare(to_system_arrays(scenario_system("subset12")), snp.Format.COMPRESSED)
@@ -167,17 +208,24 @@ def test_lean_kernel_many_steps_bit_exact(delays, policy):
     np.testing.assert_array_equal(tr.delays[-1], want_d)
 
 
-def test_full_size_formats_agree():
-    """ELL and push-Optimized reach the same state as pull-Optimized at 10^7."""
-    a = snp.synth_v1(10_000_000, with_delays=True)
-    finals = []
+@pytest.mark.parametrize("tag", ["k3", "k4"])
+def test_full_size_formats_match_oracle(tag):
+    """K3 / K4 at 10^7: every COMPRESSED variant and ELL, 4 steps under
+    FirstApplicable and SeededRandom, equal the C oracle (configuration and
+    delays)."""
+    q, steps = 10_000_000, 4
+    a = snp.synth_v1(q, with_delays=tag == "k4")
+    osys = OracleSystem.from_arrays(a)
+    want = {pol: coracle.run(osys, steps, pol, 240804343)[1:] for pol in (0, 1)}
     for fmt, variant in [(snp.Format.COMPRESSED, "tiled"), (snp.Format.COMPRESSED, "pull"),
                          (snp.Format.COMPRESSED, "push"), (snp.Format.ELL, "auto")]:
         prep = snp.prepare(a, fmt, variant=variant)
-        finals.append(snp.run_final(prep, snp.SimOptions(max_steps=4)).config)
+        for pol, sel in ((0, snp.FirstApplicable()), (1, snp.SeededRandom(240804343))):
+            res = snp.run_final(prep, snp.SimOptions(max_steps=steps, selection=sel))
+            assert res.steps == steps and res.halt_reason is snp.HaltReason.STEP_LIMIT
+            np.testing.assert_array_equal(res.config, want[pol][0], err_msg=f"{fmt} {variant} {pol}")
+            np.testing.assert_array_equal(res.delays, want[pol][1], err_msg=f"{fmt} {variant} {pol}")
         del prep
-    for other in finals[1:]:
-        np.testing.assert_array_equal(finals[0], other)
 
 
 # -- phase functions (test_engine.py:66-259) --------------------------------------------------
@@ -495,3 +543,31 @@ def test_multi_amount_production_paths(pmax):
         res = snp.run_final(prep, snp.SimOptions(max_steps=15, selection=snp.SeededRandom(21)))
         np.testing.assert_array_equal(res.config, want_c, err_msg=variant)
         np.testing.assert_array_equal(res.delays, want_d, err_msg=variant)
+
+
+@pytest.mark.parametrize("mode", ["binned", "atomic", "unfused"])
+@pytest.mark.parametrize("pmax", [1, 300])
+def test_push_step_kernels_match_oracle(mode, pmax, monkeypatch):
+    """The three ways a push-format run steps (include/snpb200.h SNP_PUSH_*):
+    binned deliveries (u16 slots for a common amount, u32 slot|amount
+    otherwise), L2 atomics, and the unfused step + scatter kernels -- ELL and
+    COMPRESSED-push, with delays, SeededRandom, vs the C oracle: 20 steps of
+    final state and 8 FULL trace rows."""
+    from conftest import multi_amount_system
+    if mode != "binned":
+        monkeypatch.setenv("SNPB200_PUSH", mode)
+    q = 200_000
+    a = snp.synth_v1(q, with_delays=True) if pmax == 1 else multi_amount_system(q, pmax)
+    osys = OracleSystem.from_arrays(a)
+    _, want_c, want_d = coracle.run(osys, 20, 1, 21)
+    ref, _, _ = coracle.run(osys, 8, 1, 21, trace_rows=9)
+    for fmt, var in ((snp.Format.ELL, "auto"), (snp.Format.COMPRESSED, "push")):
+        prep = snp.prepare(a, fmt, variant=var)
+        assert snp._native.PUSH_KERNELS[prep.engine.info["push_kernel"]] == mode
+        res = snp.run_final(prep, snp.SimOptions(max_steps=20, selection=snp.SeededRandom(21)))
+        np.testing.assert_array_equal(res.config, want_c, err_msg=f"{fmt} {mode}")
+        np.testing.assert_array_equal(res.delays, want_d, err_msg=f"{fmt} {mode}")
+        tr = snp.simulate_prepared(prep, snp.SimOptions(max_steps=8, selection=snp.SeededRandom(21),
+                                                        record=snp.RecordLevel.FULL))
+        assert trace_digest(tr.configs, tr.delays, tr.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
+        del prep

@@ -223,3 +223,10 @@ def test_selection_hash_vector_matches_scalar():
     assert choose_index(snp.FirstApplicable(), 0, 0, 9) == 0
     kat = golden_json("mix64_kat.json")
     assert all(mix64(s, k, n) == w for s, k, n, w in kat)
+
+
+def test_phase_cache_key_handles_empty_arrays():
+    """Zero-size inputs (e.g. a 0-row SynapseMatrix) still get a content key."""
+    from paper_2408_04343_b200.engine import _content_key
+    assert _content_key(np.zeros((0, 3), np.int64)) != _content_key(np.zeros((3, 0), np.int64))
+    assert _content_key(np.zeros(0, np.int64), np.arange(3)) == _content_key(np.zeros(0, np.int64), np.arange(3))

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), f"{name} missing from {nat.LIB_PATH}"
     assert {n for n, _, _ in nat.SIGNATURES} == set(names)
-    assert lib.snp_abi_version() == 5
+    assert lib.snp_abi_version() == 6
 
 
 def test_struct_layouts_match_header(tmp_path):

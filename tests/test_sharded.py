@@ -205,7 +205,9 @@ def test_protocol_over_gloo_negative_on_last_and_mid_step(extra):
 def _run_sharded_on_one_gpu(arrays, world, max_steps, selection=snp.FirstApplicable()):
     q = arrays.neuron_count
     L = shd.shard_layout(q, world)
-    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world) for r in range(world)]
+    span = shd.p_range(arrays.rules)
+    L = shd.shard_layout(q, world, shd.exchange_width(*span)[0])
+    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world, p_span=span) for r in range(world)]
     views = [r.slots_torch() for r in ranks]
     for r in ranks:
         r.engine.begin()
@@ -261,7 +263,8 @@ def _run_p2p_on_one_gpu(arrays, world, max_steps, selection=snp.FirstApplicable(
     before any rank's step k+1 waits for them)."""
     q = arrays.neuron_count
     L = shd.shard_layout(q, world)
-    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world) for r in range(world)]
+    span = shd.p_range(arrays.rules)
+    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, L, r), q, r, world, p_span=span) for r in range(world)]
     shd.ShardedEngine.connect_local(ranks)
     stream = torch.cuda.Stream()  # one non-default stream: strictly round-robin execution
     for r in ranks:
@@ -305,13 +308,50 @@ def test_peer_exchange_matches_single(world, case):
         assert halt == 2 and cfg[600:].tolist() == list(range(1, 301))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("pmax", [3, 300])
+@pytest.mark.parametrize("exchange", ["allgather", "p2p"])
+def test_row_partition_multi_amount(world, pmax, exchange):
+    """Produced amounts that differ between rules: the exchange carries u8 /
+    u16 P elements instead of bits; 2 and 4 ranks equal the single engine and
+    the C oracle."""
+    from conftest import multi_amount_system
+    arrays = multi_amount_system(60_000, pmax)
+    span = shd.p_range(arrays.rules)
+    assert shd.exchange_width(*span)[0] == (8 if pmax < 256 else 16)
+    sel, L = snp.SeededRandom(21), 12
+    want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED), snp.SimOptions(max_steps=L, selection=sel))
+    _, oc, od = coracle.run(OracleSystem.from_arrays(arrays), L, 1, 21)
+    np.testing.assert_array_equal(want.config, oc)
+    run = _run_sharded_on_one_gpu if exchange == "allgather" else _run_p2p_on_one_gpu
+    cfg, dly, steps, halt = run(arrays, world, L, sel)
+    np.testing.assert_array_equal(cfg, oc)
+    np.testing.assert_array_equal(dly, od)
+    assert steps == want.steps == L
+
+
+def test_exchange_width_rule():
+    assert shd.exchange_width(1, 1) == (1, 1)
+    assert shd.exchange_width(0, 0) == (1, 1)
+    assert shd.exchange_width(2, 2) == (1, 2)
+    assert shd.exchange_width(1, 3) == (8, 3)
+    assert shd.exchange_width(1, 255) == (8, 255)
+    assert shd.exchange_width(1, 256) == (16, 256)
+    assert shd.exchange_width(1, 70_000) == (32, 70_000)
+    L = shd.shard_layout(10_000, 4, 8)
+    assert L.hdr == 16 and L.chunk_words == L.nl // 4 + 4
+    x = L.xpos(np.arange(10_000))
+    assert (np.diff(x) > 0).all() and ((x % (L.nl + L.hdr)) < L.nl).all()
+
+
 def _p2p_rank_proc(rank, world, q, steps, conn, out):
     """One rank of a 2-process peer exchange on the same device (CUDA IPC)."""
     import paper_2408_04343_b200 as snp_
     from paper_2408_04343_b200 import sharded as shd_
     arrays = snp_.synth_v1(q, with_delays=True)
     L = shd_.shard_layout(q, world)
-    sh = shd_.ShardedEngine(shd_.local_arrays(arrays, L, rank), q, rank, world)
+    sh = shd_.ShardedEngine(shd_.local_arrays(arrays, L, rank), q, rank, world, p_span=shd_.p_range(arrays.rules))
     conn.send(sh.ipc_handle())
     other = conn.recv()
     handles = [None] * world
@@ -423,7 +463,8 @@ def test_sharded_negative_spikes_reported(world, exchange, extra):
         snp.run_final(snp.prepare(a, snp.Format.COMPRESSED), snp.SimOptions(max_steps=L + extra))
     q = a.neuron_count
     lay = shd.shard_layout(q, world)
-    ranks = [shd.ShardedEngine(shd.local_arrays(a, lay, r), q, r, world) for r in range(world)]
+    ranks = [shd.ShardedEngine(shd.local_arrays(a, lay, r), q, r, world, p_span=shd.p_range(a.rules))
+             for r in range(world)]
     if exchange == "p2p":
         shd.ShardedEngine.connect_local(ranks)
         stream = torch.cuda.Stream()
