@@ -49,8 +49,10 @@ enum { SNP_FMT_SPARSE = 0, SNP_FMT_ELL = 1, SNP_FMT_COMPRESSED = 2 };
  * in-edge segments and shared-memory accumulation; PULL = per-destination
  * CSR gather; PUSH = the paper's Alg. 5 scatter with atomics. */
 enum { SNP_VARIANT_AUTO = 0, SNP_VARIANT_PULL = 1, SNP_VARIANT_PUSH = 2, SNP_VARIANT_TILED = 3,
-       SNP_VARIANT_TILED2 = 4 };  /* TILED2: two-pass receive (pass 1 per source window, then tiles);
+       SNP_VARIANT_TILED2 = 4,    /* TILED2: two-pass receive (pass 1 per source window, then tiles);
                                      for sources spread far beyond the engine's rows (10^8, partitions) */
+       SNP_VARIANT_SMALL = 5 };   /* SMALL: q <= 16384 -- one CTA runs a whole loop segment per launch
+                                     (no per-step launch); AUTO picks it for small systems */
 
 /* selection.py:21-31 */
 enum { SNP_POLICY_FIRST = 0, SNP_POLICY_SEEDED = 1 };

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 SNP_OK, SNP_ERR_NEGATIVE, SNP_ERR_BAD_ARG, SNP_ERR_CUDA, SNP_ERR_CAPACITY = range(5)
 SNP_FMT_SPARSE, SNP_FMT_ELL, SNP_FMT_COMPRESSED = range(3)
-SNP_VARIANT_AUTO, SNP_VARIANT_PULL, SNP_VARIANT_PUSH, SNP_VARIANT_TILED, SNP_VARIANT_TILED2 = range(5)
+SNP_VARIANT_AUTO, SNP_VARIANT_PULL, SNP_VARIANT_PUSH, SNP_VARIANT_TILED, SNP_VARIANT_TILED2, SNP_VARIANT_SMALL = range(6)
 SNP_REC_CONFIGS, SNP_REC_DELAYS, SNP_REC_SPIKING, SNP_REC_DIGEST = 1, 2, 4, 8
 SNP_RUNNING, SNP_HALT_STEP_LIMIT, SNP_HALT_NO_APPLICABLE, SNP_HALT_NEGATIVE, SNP_HALT_EXCHANGE = range(5)
 SNP_IPC_HANDLE_BYTES = 64

@@ -178,7 +178,8 @@ struct DevSys {
     int bin_ntiles;
     unsigned long long bin_magic;  // ceil(2^64 / bin_T): floor(x / bin_T) = umul64hi(x, bin_magic) for x < 2^31
     int bin_amount;                // UNIT entries: the common amount of every delivery
-    const uint32_t* bin_off;       // [ntiles + 1] region starts (entries, multiples of 8)
+    const uint32_t* bin_off;       // [ntiles + 1] main region starts (entries, multiples of 8)
+    const uint32_t* bin_ooff;      // [ntiles + 1] overflow region starts (same buffer, after the main regions)
 };
 
 struct DevState {
@@ -189,7 +190,7 @@ struct DevState {
     long long* recv;          // push/dense accumulation
     void* rbuf[2];            // fused push (push_step_kernel): receive buffers by step parity, int32 or int64
     void* bins[2];            // binned push: bin entries by step parity (u16 slots or u32 slot|amount)
-    uint32_t* bin_fill[2];    // binned push: entries written into each tile's region, by step parity
+    uint32_t* bin_fill[2];    // binned push: [2 * ntiles] entries written into each tile's main / overflow region, by step parity
     uint32_t* list[2];        // fired rules (dense) / heavy queue (push), by parity
     Ctrl* ctrl;
     long long* tr_cfg;        // [tr_rows][q]
@@ -1150,6 +1151,16 @@ static_assert(sizeof(StageHdr) <= kHdrBytes, "header fits");
 
 // Stage payload offsets (from the stage start)
 constexpr uint32_t kPayload = kHdrBytes;
+// Phase-2 stages use one fixed layout whatever their destination count n <=
+// kSub (payload-relative): Ĉ int64[kSub] at 0, delay state int32[kSub] at
+// kP2Ds, rule offsets u32[kSub + 1] at kP2Roff (irregular systems only), rule
+// words at kP2Rules(rpn) -- constant addresses for the consumers.
+constexpr uint32_t kP2Ds = (uint32_t)kSub * 8u;
+constexpr uint32_t kP2Roff = (uint32_t)kSub * 12u;
+__host__ __device__ constexpr uint32_t kP2Rules(bool regular) {
+    return regular ? kP2Roff : kP2Roff + ((((uint32_t)kSub + 1u) * 4u + 15u) & ~15u);
+}
+static_assert(kP2Ds % 16 == 0 && kP2Roff % 16 == 0, "16-byte aligned bulk-copy destinations");
 
 __device__ __forceinline__ uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -1422,10 +1433,10 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                             h->rstaged = f4 ? 1u : 0u;
                             mbar_expect_tx(&full_bar[b], b_cfg + b_ds + b_roff + f4);
                             bulk_g2s(buf + kPayload, st.cfg + j0, b_cfg, &full_bar[b]);
-                            bulk_g2s(buf + kPayload + b_cfg, st.ds + j0, b_ds, &full_bar[b]);
-                            if (b_roff) bulk_g2s(buf + kPayload + b_cfg + b_ds, s.roff + j0, b_roff, &full_bar[b]);
+                            bulk_g2s(buf + kPayload + kP2Ds, st.ds + j0, b_ds, &full_bar[b]);
+                            if (b_roff) bulk_g2s(buf + kPayload + kP2Roff, s.roff + j0, b_roff, &full_bar[b]);
                             if (f4)
-                                bulk_g2s(buf + kPayload + b_cfg + b_ds + b_roff,
+                                bulk_g2s(buf + kPayload + kP2Rules(s.rpn != 0),
                                          rw_src + (size_t)f3 * rw_size, f4, &full_bar[b]);
                         }
                     }
@@ -1559,7 +1570,73 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
             consumer_sync(kTileThreads);  // acc complete
 
             // ---- phase 2: finish step k-1, select step k (one destination per thread)
-            for (;;) {
+            if (LEAN && TINY && kP2Rep == 1 && s.rpn > 0 && s.rpn <= 4 && (s.dbg & 2) == 0) {
+                // Regular systems with <= 4 rules per neuron (implicit offsets,
+                // no heavy neurons): the stage addresses are constants and the
+                // per-stage bookkeeping is a header load, the wait and one
+                // arrival -- the generic loop below spends more instructions on
+                // that than on the selection itself (ncu source view, K3).
+                const uint32_t nr = (uint32_t)s.rpn;
+                const int li = threadIdx.x;
+                for (;;) {
+                    const int b = cb;
+                    const uint8_t* buf = ring + b * kStageBytes;
+                    mbar_wait(&full_bar[b], cround & 1u);
+                    if (++cb == nst) {
+                        cb = 0;
+                        ++cround;
+                    }
+                    const uint4 hd = *reinterpret_cast<const uint4*>(buf);      // kind, last, first, n
+                    const uint2 hr = *reinterpret_cast<const uint2*>(buf + 24);  // r_al, rstaged
+                    const uint32_t n = hd.w;
+                    const bool active = li < (int)n;
+                    const int i = (int)hd.z + li;
+                    const long long j = d0 + i;
+                    long long Cprev = 0;
+                    int dsv = 0;
+                    alignas(16) uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                    if (active) {
+                        Cprev = reinterpret_cast<const long long*>(buf + kPayload)[li];
+                        dsv = reinterpret_cast<const int*>(buf + kPayload + kP2Ds)[li];
+                        const uint32_t r0 = nr * (uint32_t)j;
+                        if (hr.y) {
+                            const uint32_t* rp =
+                                reinterpret_cast<const uint32_t*>(buf + kPayload + kP2Rules(true)) + (r0 - hr.x);
+                            if (nr == 4) {
+                                const uint4 v = *reinterpret_cast<const uint4*>(rp);  // r_al = 4 * first neuron
+                                wv[0] = v.x, wv[1] = v.y, wv[2] = v.z, wv[3] = v.w;
+                            } else {
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) wv[x] = rp[x];  // words past nr are masked off
+                            }
+                        } else {
+                            for (uint32_t x = 0; x < nr; ++x) wv[x] = __ldg(s.rw4 + r0 + x);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[b]);
+                    long long pval = 0;
+                    if (active) {
+                        long long C = Cprev;
+                        if (ds_open(dsv)) {
+                            const uint32_t gsum = tile_acc_get<CB>(acc, i);
+                            C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
+                        }
+                        const int D = ds_next(dsv);
+                        pval = lean_commit4<PM, true>(s, st, ctl, cx, j, nr, wv, C, D, sel && D == 0, t_fired, t_closed,
+                                                      t_neg);
+                    }
+                    if (sel && PM == P_BIT) {
+                        const unsigned int bits = __ballot_sync(0xffffffffu, pval > 0);
+                        if (lane == 0 && warp * 32 < (int)n) {
+                            const long long wd = (j + s.xbase) >> 5;
+                            Pzero[wd] = 0u;
+                            Pcur[wd] = bits;
+                        }
+                    }
+                    if (hd.y) break;
+                }
+            } else for (;;) {
                 const int b = cb;
                 const uint8_t* buf = ring + b * kStageBytes;
                 mbar_wait(&full_bar[b], cround & 1u);
@@ -1570,12 +1647,10 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                 const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
                 const uint32_t n = h->n, last = h->last, first = h->first, r_al = h->r_al;
                 const bool rstaged = h->rstaged != 0;  // staged words are tiny words when TINY
-                const uint32_t b_cfg = round16(n * 8u), b_ds = round16(n * 4u),
-                               b_roff = s.rpn ? 0u : round16((n + 1u) * 4u);
                 const long long* cfg_s = reinterpret_cast<const long long*>(buf + kPayload);
-                const int* ds_s = reinterpret_cast<const int*>(buf + kPayload + b_cfg);
-                const uint32_t* roff_s = reinterpret_cast<const uint32_t*>(buf + kPayload + b_cfg + b_ds);
-                const Raw* rules_s = reinterpret_cast<const Raw*>(buf + kPayload + b_cfg + b_ds + b_roff);
+                const int* ds_s = reinterpret_cast<const int*>(buf + kPayload + kP2Ds);
+                const uint32_t* roff_s = reinterpret_cast<const uint32_t*>(buf + kPayload + kP2Roff);
+                const Raw* rules_s = reinterpret_cast<const Raw*>(buf + kPayload + kP2Rules(s.rpn != 0));
                 bool released = false;
                 // kP2Rep destinations per consumer thread (li, li + kTileThreads, ...)
 #pragma unroll 1
@@ -2094,44 +2169,58 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const
 //
 // Destinations are cut into bin_ntiles tiles of bin_T.  One kernel per step k;
 // a CTA owns tiles and for each tile:
-//   A. receive: the tile's bin entries written during step k-1 (region
-//      bin_off[t], bin_fill[(k+1)&1][t] entries) -> 8/16/32-bit counters in
-//      shared memory;
+//   A. receive: the tile's bin entries written during step k-1 (main region:
+//      whole 16-byte units; overflow region: single entries) -> 8/16/32-bit
+//      counters in shared memory;
 //   B. for 1024 destinations at a time: finish step k-1 (C += open ? recv),
 //      update delays, select step k (sv_calc), consume (row 0 of the ELL
 //      column, applied at selection like COMPRESSED);
-//   C. walk the fired neurons' columns (ELL rows 1.., 16-byte coalesced loads
-//      with an L2 evict-first hint; Optimized: the out-adjacency), and stage
-//      each delivery's entry (u16 slot when every delivery carries the same
+//   C. walk the fired neurons' columns (ELL rows 1.., 16-byte loads with an
+//      L2 evict-first hint; Optimized: the out-adjacency) -- each lane its own
+//      column when the warp's columns are of similar length, else 32 chunks at
+//      a time over the warp's concatenated columns -- and stage each
+//      delivery's entry (u16 slot when every delivery carries the same
 //      amount, else u32 slot << 15 | amount) in a per-destination-tile bucket
-//      of kBinCap entries in shared memory; full buckets spill single entries
-//      to global memory (rare), and after each 1024-destination chunk every
-//      bucket is flushed with one reservation (atomicAdd on the tile's fill
-//      counter) and coalesced stores.
+//      of kCap entries in shared memory; a full bucket sends single entries to
+//      the tile's overflow region;
+//   D. every kWin chunks (and at the tile's end) each bucket is flushed to the
+//      tile's main region with one reservation and 16-byte stores, padded to
+//      whole 16-byte units with entries that add nothing (slot T, the dummy
+//      counter / amount 0).
 // The bins of step k are complete at the kernel boundary; kernel k+1 reads
-// them.  Each tile's region holds the most deliveries its destinations can
-// receive in one step (their in-degrees), checked on every reservation.
+// them.  Region sizes: main = the tile's in-degree sum + the padding of every
+// possible flush, overflow = the in-degree sum (checked on every reservation).
 
 constexpr int kBinThreads = 1024;
-constexpr int kBinCap = 64;      // staged entries per destination tile per chunk
 constexpr int kBinUnroll = 4;    // column chunks in flight per lane
 
 template <bool UNIT>
 struct BinEntry {
     using T = uint32_t;
+    static constexpr int kCap = 64;   // staged entries per destination tile
+    static constexpr int kWin = 1;    // 1024-destination chunks per flush
+    static constexpr int kVec = 4;    // entries per 16-byte unit
 };
 template <>
 struct BinEntry<true> {
     using T = uint16_t;
+    static constexpr int kCap = 128;
+    static constexpr int kWin = 2;
+    static constexpr int kVec = 8;
 };
+// flushes per step into one tile are at most ceil(q / (kBinThreads * kWin)) + ntiles
+__host__ __device__ constexpr long long bin_flush_dests(bool unit) { return unit ? 2048 : 1024; }
 
 template <int CB>
 __host__ __device__ constexpr int bin_acc_words(int T) { return (acc_words<CB>(T) + 3) & ~3; }
 
 template <bool ELL, bool WIDE, bool UNIT, int CB>
 __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __grid_constant__ DevSys s, DevState st) {
-    using E = typename BinEntry<UNIT>::T;
-    extern __shared__ __align__(16) uint8_t smem[];
+    using BE = BinEntry<UNIT>;
+    using E = typename BE::T;
+    constexpr int kCap = BE::kCap, kWin = BE::kWin, kVec = BE::kVec;
+    constexpr uint32_t kEsz = sizeof(E);
+    extern __shared__ __align__(128) uint8_t smem[];
     const int NT = s.bin_ntiles, T = s.bin_T;
     uint32_t* acc = reinterpret_cast<uint32_t*>(smem);
     uint32_t* cnt = acc + bin_acc_words<CB>(T);
@@ -2152,7 +2241,10 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
     uint32_t* fill_out = (k & 1) ? st.bin_fill[1] : st.bin_fill[0];
     const uint64_t pol = evict_first_policy();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t acc_s = smem_u32(acc);
+    // shared-window addresses, computed once (the bucket code is per delivery)
+    const uint32_t acc_s = smem_u32(acc), cnt_s = smem_u32(cnt), stage_s = smem_u32(stage);
+    const unsigned long long magic = s.bin_magic;
+    const E pad = UNIT ? (E)T : (E)0;  // adds to the dummy counter / adds 0
 
     unsigned int stat[ST_COUNT];
 #pragma unroll
@@ -2168,13 +2260,13 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
         // ---- A. receive the deliveries of step k-1 into the tile's counters
         for (int i = threadIdx.x; i < acc_words<CB>(T); i += kBinThreads) acc[i] = 0;
         __syncthreads();
-        {
-            const uint32_t nin = k > 0 ? *(volatile uint32_t*)(fill_in + tile) : 0u;
-            const E* src = bin_in + __ldg(s.bin_off + tile);  // 16-byte aligned
-            constexpr int kPer = 16 / (int)sizeof(E);
-            const uint32_t nv = nin / kPer;
+        if (k > 0) {
+            const uint32_t nin = *(volatile uint32_t*)(fill_in + tile);  // whole 16-byte units
+            const uint32_t nov = *(volatile uint32_t*)(fill_in + NT + tile);
+            const uint4* src = reinterpret_cast<const uint4*>(bin_in + __ldg(s.bin_off + tile));
+            const uint32_t nv = nin / kVec;
             for (uint32_t v = threadIdx.x; v < nv; v += kBinThreads) {
-                const uint4 w = __ldcs(reinterpret_cast<const uint4*>(src) + v);
+                const uint4 w = __ldcs(src + v);
                 const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                 for (int x = 0; x < 4; ++x) {
@@ -2186,16 +2278,20 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
                     }
                 }
             }
-            for (uint32_t i = nv * kPer + threadIdx.x; i < nin; i += kBinThreads) {
-                const uint32_t e = src[i];
+            const E* osrc = bin_in + __ldg(s.bin_ooff + tile);
+            for (uint32_t i = threadIdx.x; i < nov; i += kBinThreads) {
+                const uint32_t e = osrc[i];
                 if (UNIT) tile_acc_add_slot<CB>(acc_s, e, 1u);
                 else tile_acc_add_slot<CB>(acc_s, e >> 15, e & 0x7fffu);
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0 && k > 0) fill_in[tile] = 0;  // the region is refilled in step k+1
-        // ---- B + C, 1024 destinations at a time
-        for (int c0 = 0; c0 < nd; c0 += kBinThreads) {
+        if (threadIdx.x == 0 && k > 0) {  // the regions are refilled in step k+1
+            fill_in[tile] = 0;
+            fill_in[NT + tile] = 0;
+        }
+        // ---- B + C (+ D every kWin chunks), 1024 destinations at a time
+        for (int c0 = 0, win = 0; c0 < nd; c0 += kBinThreads, ++win) {
             const int li = c0 + threadIdx.x;
             const long long j = d0 + li;
             int r = -1;
@@ -2242,77 +2338,114 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
                     edges += len;
                 }
             }
-            uint32_t incl = nch;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            const uint32_t excl = incl - nch;
             const int amount = (int)pval;
-            auto deliver = [&](int t, int a) {
-                const uint32_t dt = (uint32_t)__umul64hi((unsigned long long)(uint32_t)t, s.bin_magic);
-                const uint32_t slot = (uint32_t)t - dt * (uint32_t)T;
-                const E e = UNIT ? (E)slot : (E)((slot << 15) | (uint32_t)a);
-                const uint32_t pos = atomicAdd(cnt + dt, 1u);
-                if (pos < (uint32_t)kBinCap) {
-                    stage[dt * kBinCap + pos] = e;
-                } else {  // bucket full: one entry straight to the tile's region
-                    const uint32_t g = atomicAdd(fill_out + dt, 1u);
-                    const uint32_t o = __ldg(s.bin_off + dt);
-                    if (o + g < __ldg(s.bin_off + dt + 1)) bin_out[o + g] = e;
+            auto deliver = [&](uint32_t t, uint32_t a) {
+                const uint32_t dt = (uint32_t)__umul64hi((unsigned long long)t, magic);
+                const uint32_t slot = t - dt * (uint32_t)T;
+                const uint32_t e = UNIT ? slot : ((slot << 15) | a);
+                uint32_t pos;
+                asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(cnt_s + dt * 4u) : "memory");
+                if (pos < (uint32_t)kCap) {
+                    const uint32_t addr = stage_s + (dt * (uint32_t)kCap + pos) * kEsz;
+                    if (UNIT) asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)e) : "memory");
+                    else asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(e) : "memory");
+                } else {  // bucket full: one entry to the tile's overflow region
+                    const uint32_t g = atomicAdd(fill_out + NT + dt, 1u);
+                    const uint32_t o = __ldg(s.bin_ooff + dt);
+                    if (o + g < __ldg(s.bin_ooff + dt + 1)) bin_out[o + g] = (E)e;
                     else t_over = true;
                 }
             };
-            for (uint32_t g0 = 0; g0 < total; g0 += 32 * kBinUnroll) {
-                int4 v[kBinUnroll];
-                uint32_t cc[kBinUnroll], ln[kBinUnroll];
-                int am[kBinUnroll];
+            const uint32_t total = __reduce_add_sync(0xffffffffu, nch);
+            const uint32_t mx = __reduce_max_sync(0xffffffffu, nch);
+            if (mx * 32u <= 2u * total) {
+                // lane-own columns: lane l walks its column, kBinUnroll chunks in flight
+                for (uint32_t cb0 = 0; cb0 < mx; cb0 += kBinUnroll) {
+                    int4 v[kBinUnroll];
 #pragma unroll
-                for (int u = 0; u < kBinUnroll; ++u) {
-                    const uint32_t g = g0 + u * 32 + lane;
-                    int L = 0;
-#pragma unroll
-                    for (int w = 16; w > 0; w >>= 1) {
-                        const uint32_t x = __shfl_sync(0xffffffffu, incl, L + w - 1);
-                        if (x <= g) L += w;
+                    for (int u = 0; u < kBinUnroll; ++u) {
+                        const uint32_t c = cb0 + u;
+                        v[u] = make_int4(-1, 0, -1, 0);
+                        if (c < nch) {
+                            if (ELL) v[u] = ld_stream16(s.ell + base + 2 * c, pol);
+                            else v[u].x = (int)ld_stream4(s.sdst + base + c, pol);
+                        }
                     }
-                    cc[u] = g - __shfl_sync(0xffffffffu, excl, L);
-                    const long long b = __shfl_sync(0xffffffffu, base, L);
-                    ln[u] = __shfl_sync(0xffffffffu, len, L);
-                    am[u] = __shfl_sync(0xffffffffu, amount, L);
-                    v[u] = make_int4(-1, 0, -1, 0);
-                    if (g < total) {
-                        if (ELL) v[u] = ld_stream16(s.ell + b + 2 * cc[u], pol);
-                        else v[u].x = (int)ld_stream4(s.sdst + b + cc[u], pol);
+#pragma unroll
+                    for (int u = 0; u < kBinUnroll; ++u) {
+                        const uint32_t c = cb0 + u;
+                        if (c >= nch) continue;
+                        if (ELL) {
+                            if (c > 0) deliver((uint32_t)v[u].x, (uint32_t)v[u].y);  // row 2c (row 0 = consumption)
+                            if (2 * c + 1 < len) deliver((uint32_t)v[u].z, (uint32_t)v[u].w);
+                        } else {
+                            deliver((uint32_t)v[u].x, (uint32_t)amount);
+                        }
                     }
                 }
+            } else {
+                // uneven columns: 32 chunks at a time over the warp's concatenated columns
+                uint32_t incl = nch;
 #pragma unroll
-                for (int u = 0; u < kBinUnroll; ++u) {
-                    if (g0 + u * 32 + lane >= total) continue;
-                    if (ELL) {
-                        if (cc[u] > 0) deliver(v[u].x, v[u].y);             // row 2c (row 0 = consumption)
-                        if (2 * cc[u] + 1 < ln[u]) deliver(v[u].z, v[u].w);  // row 2c + 1
-                    } else {
-                        deliver(v[u].x, am[u]);
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const uint32_t excl = incl - nch;
+                for (uint32_t g0 = 0; g0 < total; g0 += 32 * kBinUnroll) {
+                    int4 v[kBinUnroll];
+                    uint32_t cc[kBinUnroll], ln[kBinUnroll];
+                    int am[kBinUnroll];
+#pragma unroll
+                    for (int u = 0; u < kBinUnroll; ++u) {
+                        const uint32_t g = g0 + u * 32 + lane;
+                        int L = 0;
+#pragma unroll
+                        for (int w = 16; w > 0; w >>= 1) {
+                            const uint32_t x = __shfl_sync(0xffffffffu, incl, L + w - 1);
+                            if (x <= g) L += w;
+                        }
+                        cc[u] = g - __shfl_sync(0xffffffffu, excl, L);
+                        const long long b = __shfl_sync(0xffffffffu, base, L);
+                        ln[u] = __shfl_sync(0xffffffffu, len, L);
+                        am[u] = __shfl_sync(0xffffffffu, amount, L);
+                        v[u] = make_int4(-1, 0, -1, 0);
+                        if (g < total) {
+                            if (ELL) v[u] = ld_stream16(s.ell + b + 2 * cc[u], pol);
+                            else v[u].x = (int)ld_stream4(s.sdst + b + cc[u], pol);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBinUnroll; ++u) {
+                        if (g0 + u * 32 + lane >= total) continue;
+                        if (ELL) {
+                            if (cc[u] > 0) deliver((uint32_t)v[u].x, (uint32_t)v[u].y);
+                            if (2 * cc[u] + 1 < ln[u]) deliver((uint32_t)v[u].z, (uint32_t)v[u].w);
+                        } else {
+                            deliver((uint32_t)v[u].x, (uint32_t)am[u]);
+                        }
                     }
                 }
             }
+            if ((win + 1) % kWin != 0 && c0 + kBinThreads < nd) continue;  // keep staging
             __syncthreads();
-            // flush every bucket: one reservation, coalesced stores
+            // ---- D. flush every bucket: pad to whole 16-byte units, one reservation, vector stores
             for (int dt = warp; dt < NT; dt += kBinThreads / 32) {
                 const uint32_t c = cnt[dt];
                 if (c == 0) continue;
-                const uint32_t n = min(c, (uint32_t)kBinCap);
+                const uint32_t n = min(c, (uint32_t)kCap);
+                const uint32_t np = (n + kVec - 1) & ~(uint32_t)(kVec - 1);
+                E* row = stage + dt * kCap;
+                if ((uint32_t)lane < np - n) row[n + lane] = pad;
                 uint32_t g = 0;
-                if (lane == 0) g = atomicAdd(fill_out + dt, n);
+                if (lane == 0) g = atomicAdd(fill_out + dt, np);
                 g = __shfl_sync(0xffffffffu, g, 0);
+                __syncwarp();
                 const uint32_t o = __ldg(s.bin_off + dt), cap = __ldg(s.bin_off + dt + 1) - o;
-                if (g + n > cap) {
+                if (g + np > cap) {
                     t_over = true;
-                } else {
-                    for (uint32_t i = lane; i < n; i += 32) bin_out[o + g + i] = stage[dt * kBinCap + i];
+                } else if ((uint32_t)lane < np / kVec) {
+                    reinterpret_cast<uint4*>(bin_out + o + g)[lane] = reinterpret_cast<const uint4*>(row)[lane];
                 }
                 __syncwarp();
                 if (lane == 0) cnt[dt] = 0;
@@ -2337,6 +2470,193 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
     const bool bn = __syncthreads_or(t_neg);
     if (threadIdx.x == 0) finish_step(ctl, k, sel, bf, bc, bn, sh_neg_idx, bn ? sh_neg_val : 0);
 }
+
+// ---------------------------------------------------------------------------
+// Small systems (variant SMALL; COMPRESSED, q <= kSmallMaxQ): ONE CTA runs a
+// whole loop segment -- every step of [step, stop_at) -- in one launch, with
+// block barriers where the other variants have kernel boundaries and the
+// receive vector in shared memory.  A graph-replayed grid-wide step kernel
+// costs ~10 us per step on this B200 however little a step holds (sort
+// n <= 100 is far below a microsecond of work), so small systems were
+// launch-bound; here a step is a handful of barriers.  Step semantics are
+// step_kernel<RECV_ARRAY> + push_kernel (consumption at selection, push of
+// Alg. 5, engine.py:312-356): per step k
+//   A. finish step k-1 for every neuron (C += open ? recv, D, NegativeSpikes,
+//      trace rows) and select the <= 32-rule neurons (light_commit);
+//   B. select the > 32-rule neurons, one warp each (guard index /
+//      SeededRandom scan, as the tiled kernel's phase 3);
+//   C. push: each fired sending neuron adds p to its targets' counters
+//      (shared-memory 64-bit atomics);
+//   D. halting decision for step k (finish_step's rules), then the next step.
+constexpr int kSmallThreads = 1024;
+constexpr long long kSmallMaxQ = 16384;   // 128 KB of int64 receive counters
+
+#ifndef SNP_TEMPLATES_ONLY
+template <bool WIDE>
+__global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __grid_constant__ DevSys s, DevState st) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    long long* recv_s = reinterpret_cast<long long*>(smem);  // [q] deliveries of the previous step
+    __shared__ long long sh_neg_idx, sh_neg_val;
+    __shared__ int sh_go;
+    Ctrl* ctl = st.ctrl;
+    volatile Ctrl* vc = ctl;
+    if (vc->halted || vc->step >= vc->stop_at) {
+        if (threadIdx.x == 0) ctl->push_armed = 0;
+        return;
+    }
+    using Raw = typename RuleRaw<WIDE>::T;
+    const long long q = s.q;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long max_steps = vc->max_steps, stop_at = vc->stop_at, trace_base = vc->trace_base;
+    const int policy = vc->policy, record = vc->record;
+    const bool stats_on = vc->stats_on != 0;
+    const unsigned long long seed = vc->seed;
+    long long k = vc->step;
+    for (long long j = threadIdx.x; j < q; j += kSmallThreads) recv_s[j] = st.recv[j];
+    __syncthreads();
+    for (;;) {
+        const bool sel = k < max_steps;
+        const StepCtx cx{k, k - trace_base, q, seed, nullptr, policy, record, sel, stats_on};
+        unsigned int stat[ST_COUNT];
+#pragma unroll
+        for (int i = 0; i < ST_COUNT; ++i) stat[i] = 0;
+        bool t_fired = false, t_closed = false, t_neg = false;
+        long long neg_idx = 0x7fffffffffffffffll, neg_val = 0;
+        // ---- A
+        for (long long j = threadIdx.x; j < q; j += kSmallThreads) {
+            const uint32_t r0 = __ldg(s.roff + j), nr = __ldg(s.roff + j + 1) - r0;
+            const int dsv = st.ds[j];
+            const int D = ds_next(dsv);
+            long long C = st.cfg[j];
+            const long long rv = recv_s[j];
+            recv_s[j] = 0;
+            if (ds_open(dsv)) C += rv;
+            if (nr > kLightRules) {
+                if (C < 0 && j + s.gbase < neg_idx) {
+                    t_neg = true;
+                    neg_idx = j + s.gbase;
+                    neg_val = C;
+                }
+                if (record & REC_CONFIGS) st.tr_cfg[cx.slot * q + j] = C;
+                if (record & REC_DELAYS) st.tr_dly[cx.slot * q + j] = D;
+                t_closed |= D != 0;
+                st.cfg[j] = C;
+                st.ds[j] = D;
+                if (sel) {
+                    st.chosen[j] = -1;
+                    if (record & REC_SPIKING) st.tr_chosen[cx.slot * q + j] = -1;
+                }
+            } else {
+                const bool can_sel = sel && D == 0;
+                Raw w0{}, w1{}, w2{}, w3{};
+                if (can_sel) {
+                    if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                    if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                    if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                    if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                }
+                int r = -1;
+                long long ni = neg_idx, nv = neg_val;
+                light_commit<RECV_ARRAY, P_BIT, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D, can_sel,
+                                                                   stat, t_fired, t_closed, t_neg, ni, nv, r);
+                if (ni < neg_idx) neg_idx = ni, neg_val = nv;
+            }
+        }
+        __syncthreads();
+        // ---- B
+        if (sel) {
+            for (int h = warp; h < s.n_heavy; h += kSmallThreads / 32) {
+                const long long j = s.heavy[h];
+                if (st.ds[j] != 0) continue;  // D_k (A stored it): closed
+                const long long C = st.cfg[j];
+                const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
+                int r;
+                if (policy == 0) {
+                    const int x = heavy_first_applicable_warp(s, h, C, lane);
+                    r = x < 0 ? -1 : (int)(r0 + x);
+                    if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
+                } else {
+                    r = heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane);
+                    if (lane == 0) stat[ST_SCANNED] += r1 - r0;
+                }
+                if (lane == 0) {
+                    stat[ST_OPEN] += 1;
+                    if (r >= 0) {
+                        const uint4 wr = load_rule<WIDE>(s.rw, r);
+                        st.cfg[j] = C - (long long)wr.y;
+                        st.ds[j] = -((int)wr.w + 1);
+                        st.chosen[j] = r;
+                        t_fired = true;
+                        stat[ST_FIRED] += 1;
+                        if (wr.z > 0) {
+                            stat[ST_SENDING] += 1;
+                            if (stats_on) {
+                                const uint32_t od = __ldg(s.outdeg + j);
+                                stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
+                            }
+                        }
+                        if (record & REC_SPIKING) st.tr_chosen[cx.slot * q + j] = r;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- C
+        if (sel) {
+            for (long long j = threadIdx.x; j < q; j += kSmallThreads) {
+                const int r = st.chosen[j];
+                if (r < 0) continue;
+                const long long p = __ldg(&s.rrec[r].y);
+                if (p <= 0) continue;
+                const uint32_t e0 = __ldg(s.soff + j), e1 = __ldg(s.soff + j + 1);
+                stat[ST_EDGES] += e1 - e0;
+                for (uint32_t e = e0; e < e1; ++e)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(recv_s + __ldg(s.sdst + e)), (unsigned long long)p);
+            }
+        }
+        // ---- D
+        if (stats_on) flush_stats(ctl, stat);
+        const bool bf = __syncthreads_or(t_fired);
+        const bool bc = __syncthreads_or(t_closed);
+        if (threadIdx.x == 0) sh_neg_idx = 0x7fffffffffffffffll;
+        __syncthreads();
+        if (t_neg) atomicMin(&sh_neg_idx, neg_idx);
+        __syncthreads();
+        if (t_neg && sh_neg_idx == neg_idx) sh_neg_val = neg_val;
+        const bool bn = __syncthreads_or(t_neg);
+        if (threadIdx.x == 0) {
+            int go = 0;
+            if (vc->fault) {
+                vc->halted = 1;
+                vc->reason = HALT_FAULT;
+            } else if (bn) {
+                vc->neg_any = 1;
+                vc->neg_index = sh_neg_idx;
+                vc->neg_value = sh_neg_val;
+                vc->halted = 1;
+                vc->reason = HALT_NEGATIVE;
+            } else if (!sel) {
+                vc->halted = 1;
+                vc->reason = HALT_STEP_LIMIT;
+            } else if (!bf && !bc) {
+                vc->halted = 1;
+                vc->reason = HALT_NO_APPLICABLE;
+            } else {
+                vc->step = k + 1;
+                if (stats_on) vc->stats[ST_STEPS] += 1;
+                go = k + 1 < stop_at;
+            }
+            vc->push_armed = 0;
+            sh_go = go;
+        }
+        __syncthreads();
+        if (!sh_go) break;
+        ++k;
+    }
+    for (long long j = threadIdx.x; j < q; j += kSmallThreads) st.recv[j] = recv_s[j];
+    __threadfence();
+}
+#endif  // SNP_TEMPLATES_ONLY
 
 // Dense S.M (paper Alg. 3 over the fired rows only): blockIdx.x tiles 1024
 // columns (int4 per thread), blockIdx.y splits the fired-rule list.

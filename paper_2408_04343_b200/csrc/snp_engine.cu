@@ -141,6 +141,8 @@ struct snp_engine {
     bool bin_unit = false;     // binned push: u16 slot entries
     size_t bin_smem = 0;       // binned push: dynamic shared memory
     PrimeFn prime_fn = nullptr;
+    StepFn small_fn = nullptr;  // variant SMALL: one-CTA loop-segment kernel for runs
+    size_t small_smem = 0;
     int step_grid = 0;
     int push_grid = 0;
     int heavy_push_grid = 0;
@@ -247,7 +249,7 @@ void append_phase2_desc(const snp_engine* e, long long t, const std::vector<uint
         const uint32_t n = (uint32_t)std::min<long long>(kSub, nd - dd);
         const uint32_t rf = roff_h[d0 + dd], rl = roff_h[d0 + dd + n];
         const uint32_t r_al = e->tiny_rules ? (rf & ~3u) : (e->wide_rules ? rf : (rf & ~1u));
-        const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + (s.rpn ? 0u : r16((n + 1) * 4ull));
+        const uint32_t fixed = kPayload + kP2Rules(s.rpn != 0);
         uint32_t rb = r16((unsigned long long)(rl - r_al) * rw_size);
         if (fixed + rb > kStageBytes) rb = 0;
         StageDesc sd;
@@ -776,7 +778,8 @@ StepFn run_fn(const snp_engine* e) {
 
 // The step kernel of a run (the one-kernel push step when the engine has one).
 void launch_main(snp_engine* e) {
-    if (e->fused_fn) e->fused_fn<<<e->fused_grid, e->fused_block, e->fused_smem, e->stream>>>(e->sys, e->st);
+    if (e->small_fn) e->small_fn<<<1, kSmallThreads, e->small_smem, e->stream>>>(e->sys, e->st);
+    else if (e->fused_fn) e->fused_fn<<<e->fused_grid, e->fused_block, e->fused_smem, e->stream>>>(e->sys, e->st);
     else run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
 }
 
@@ -793,6 +796,16 @@ struct PhaseTimer {
         t = now;
     }
 };
+
+// Dynamic shared memory cap of a kernel: the device's opt-in maximum, not
+// this engine's size -- the attribute is per function, so engines of
+// different sizes in one process must not lower it under each other.
+int allow_max_smem(const void* fn, int device) {
+    int optin = 0;
+    CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    return SNP_OK;
+}
 
 int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullptr) {
     PhaseTimer tm;
@@ -966,6 +979,11 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     // --- receive path and P width
     e->variant = d->variant;
     if (e->format == SNP_FMT_COMPRESSED) {
+        // small systems: one CTA runs whole loop segments (small_run_kernel)
+        const bool small_ok = !sh && q <= kSmallMaxQ && (long long)sdst.size() + m <= (1ll << 17);
+        if (e->variant == SNP_VARIANT_AUTO && small_ok && q > 0) e->variant = SNP_VARIANT_SMALL;
+        if (e->variant == SNP_VARIANT_SMALL && (sh || q > kSmallMaxQ))
+            return fail(SNP_ERR_BAD_ARG, "variant SMALL needs an unpartitioned system of <= %lld neurons", kSmallMaxQ);
         if (e->variant == SNP_VARIANT_AUTO) {
             // tiled unless most rules sit in heavy-rule neurons (> 32 rules,
             // e.g. the sorter's detectors): those select one warp per neuron
@@ -985,7 +1003,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                 if ((double)pmax * (double)mx >= 4294967296.0) e->variant = SNP_VARIANT_PULL;
             }
         }
-        e->kind = e->variant == SNP_VARIANT_PUSH ? RECV_ARRAY : RECV_PULL;
+        e->kind = (e->variant == SNP_VARIANT_PUSH || e->variant == SNP_VARIANT_SMALL) ? RECV_ARRAY : RECV_PULL;
         e->tiled = e->variant == SNP_VARIANT_TILED || e->variant == SNP_VARIANT_TILED2;
         e->sys.tp = e->variant == SNP_VARIANT_TILED2 ? 1 : 0;
     } else {
@@ -1224,6 +1242,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     // SNPB200_PUSH=atomic forces the latter, =unfused the 3-kernel path.
     const char* push_env = getenv("SNPB200_PUSH");
     if (e->kind == RECV_ARRAY && e->format != SNP_FMT_SPARSE && s.n_heavy == 0 && q > 0 &&
+        e->variant != SNP_VARIANT_SMALL &&
         !(push_env && !strcmp(push_env, "unfused"))) {
         // per destination: deliveries it can receive in one step (each source
         // fires at most one rule) and their largest amount
@@ -1278,7 +1297,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         bool binned = false;
         if (bins_ok && recv_worst < (1ll << 32)) {
             const int cb = recv_worst < 256 ? 8 : (recv_worst < 65536 ? 16 : 32);
-            const long long tmax = unit ? 65536 : 131072;
+            const long long tmax = unit ? 65504 : 131072;  // u16 entries: the pad slot T must fit
             long long per_sm = 2;
             if (const char* env = getenv("SNPB200_BIN_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
             long long T = std::min<long long>(tmax, (ceil_div(q, per_sm * n_sm) + 31) / 32 * 32);
@@ -1286,27 +1305,41 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             const size_t esz = unit ? 2 : 4;
             const size_t acc_b = 4 * (size_t)(cb == 8 ? bin_acc_words<8>((int)T)
                                                       : (cb == 16 ? bin_acc_words<16>((int)T) : bin_acc_words<32>((int)T)));
-            const size_t smem = acc_b + 4 * (size_t)((nt + 3) & ~3ll) + (size_t)nt * kBinCap * esz;
+            const int bcap = unit ? BinEntry<true>::kCap : BinEntry<false>::kCap;
+            const size_t smem = acc_b + 4 * (size_t)((nt + 3) & ~3ll) + (size_t)nt * bcap * esz;
             if ((long long)smem + 2048 <= smem_optin) {
                 binned = true;
-                // bin regions: the in-degree of the tile's destinations, 16-byte aligned
-                std::vector<uint32_t> boff(nt + 1, 0);
+                // bin regions per tile: main = its destinations' in-degree sum
+                // plus the 16-byte padding of every flush that can reach it in
+                // one step; overflow = the in-degree sum (full buckets)
+                const unsigned long long pads =
+                    8ull * (unsigned long long)(ceil_div(q, bin_flush_dests(unit)) + nt);
+                std::vector<unsigned long long> deg(nt, 0);
+                for (long long t = 0; t < nt; ++t)
+                    for (long long jj = t * T; jj < std::min<long long>(q, (t + 1) * T); ++jj) deg[t] += ind[jj];
+                std::vector<uint32_t> boff(nt + 1, 0), ooff(nt + 1, 0);
                 unsigned long long tot = 0;
                 for (long long t = 0; t < nt; ++t) {
-                    unsigned long long c = 0;
-                    for (long long jj = t * T; jj < std::min<long long>(q, (t + 1) * T); ++jj) c += ind[jj];
                     boff[t] = (uint32_t)tot;
-                    tot += (c + 7) & ~7ull;
+                    tot += ((deg[t] + 7) & ~7ull) + pads;
                     if (tot >= (1ull << 32) - 8) return fail(SNP_ERR_CAPACITY, "push bins exceed 2^32 entries");
                 }
                 boff[nt] = (uint32_t)tot;
-                uint32_t* d_boff;
+                for (long long t = 0; t < nt; ++t) {
+                    ooff[t] = (uint32_t)tot;
+                    tot += deg[t];
+                    if (tot >= (1ull << 32) - 8) return fail(SNP_ERR_CAPACITY, "push bins exceed 2^32 entries");
+                }
+                ooff[nt] = (uint32_t)tot;
+                uint32_t *d_boff, *d_ooff;
                 TRY(upload(e, &d_boff, boff));
+                TRY(upload(e, &d_ooff, ooff));
+                s.bin_ooff = d_ooff;
                 for (int i = 0; i < 2; ++i) {
                     uint4* bb;
                     TRY(e->alloc(&bb, (long long)(tot * esz + 15) / 16 + 1));
                     st.bins[i] = bb;
-                    TRY(e->alloc(&st.bin_fill[i], nt));
+                    TRY(e->alloc(&st.bin_fill[i], 2 * nt));
                 }
                 s.bin_T = (int)T;
                 s.bin_ntiles = (int)nt;
@@ -1325,7 +1358,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                 else e->fused_fn = w ? (unit ? SNP_BIN_PICK(false, true, true) : SNP_BIN_PICK(false, true, false))
                                      : (unit ? SNP_BIN_PICK(false, false, true) : SNP_BIN_PICK(false, false, false));
 #undef SNP_BIN_PICK
-                CU(cudaFuncSetAttribute(e->fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                TRY(allow_max_smem((const void*)e->fused_fn, e->device));
             }
         }
         if (!binned) {
@@ -1411,6 +1444,11 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         }
     } else if (e->format == SNP_FMT_COMPRESSED) {
         pick_fns<RECV_ARRAY, P_BIT, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn);
+        if (e->variant == SNP_VARIANT_SMALL) {
+            e->small_fn = e->wide_rules ? small_run_kernel<true> : small_run_kernel<false>;
+            e->small_smem = (size_t)std::max<long long>(1, q) * 8;
+            TRY(allow_max_smem((const void*)e->small_fn, e->device));
+        }
     } else if (e->format == SNP_FMT_ELL) {
         pick_fns<RECV_ARRAY, P_BIT, false, false>(e->wide_rules, &e->step_fn, &e->prime_fn);
     } else {
@@ -1425,8 +1463,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                        (size_t)(e->cbits == 8 ? acc_words<8>(s.tile)
                                                  : (e->cbits == 16 ? acc_words<16>(s.tile) : acc_words<32>(s.tile))) *
                            sizeof(uint32_t);
-        CU(cudaFuncSetAttribute(e->step_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
-        CU(cudaFuncSetAttribute(e->lean_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->step_smem));
+        TRY(allow_max_smem((const void*)e->step_fn, e->device));
+        TRY(allow_max_smem((const void*)e->lean_fn, e->device));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, e->step_block, e->step_smem));
         const long long resident = (long long)std::max(1, per_sm) * std::max(1, n_sm);
         e->step_grid = (int)std::min<long long>(s.n_tiles, resident);
@@ -1482,6 +1520,10 @@ int launch_push_tail(snp_engine* e, long long* row_visits = nullptr) {
 }
 
 int launch_step(snp_engine* e, long long* row_visits = nullptr) {
+    if (e->small_fn) {  // one launch runs the rest of the segment (up to Ctrl.stop_at)
+        launch_main(e);
+        return 1;
+    }
     int n = 1 + launch_pass1(e);
     launch_main(e);
     return n + launch_push_tail(e, row_visits);
@@ -1521,7 +1563,7 @@ int reset_state(snp_engine* e) {
         CU(cudaMemsetAsync(st.recv, 0, std::max<long long>(1, q) * 8, e->stream));
         if (e->fused_fn && e->bin_cb) {
             for (int i = 0; i < 2; ++i)
-                CU(cudaMemsetAsync(st.bin_fill[i], 0, (size_t)std::max(1, e->sys.bin_ntiles) * 4, e->stream));
+                CU(cudaMemsetAsync(st.bin_fill[i], 0, (size_t)std::max(1, e->sys.bin_ntiles) * 8, e->stream));
         } else if (e->fused_fn) {
             for (int i = 0; i < 2; ++i)
                 CU(cudaMemsetAsync(st.rbuf[i], 0, std::max<long long>(1, q) * (e->recv64 ? 8 : 4), e->stream));
@@ -1757,7 +1799,10 @@ int snp_advance(snp_engine* e, const snp_run_opts* o, int64_t n_steps, snp_trace
         c.stop_at = k0 + seg;
         c.trace_base = k0;
         TRY(push_ctrl(e));
-        if (o->use_graph) {
+        if (e->small_fn) {
+            launch_main(e);
+            launches += 1;
+        } else if (o->use_graph) {
             TRY(ensure_graph(e, chunk));
             CU(cudaGraphLaunch(e->graph, e->stream));
             launches += chunk * kernels_per_step(e);
@@ -1875,7 +1920,20 @@ int snp_time_steps(snp_engine* e, const snp_run_opts* o, int64_t steps, double* 
     c.stop_at = c.step + steps;
     TRY(push_ctrl(e));
     long long launches = 0;
-    if (kernel_ms) {
+    if (e->small_fn) {
+        // one launch runs all `steps` (kernel time = the whole segment / steps)
+        CU(cudaEventRecord(e->ev0, e->stream));
+        launch_main(e);
+        launches = 1;
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(e->ev1, e->stream));
+        CU(cudaEventSynchronize(e->ev1));
+        if (kernel_ms) {
+            float ms = 0;
+            CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+            *kernel_ms = steps > 0 ? ms / steps : 0.0;
+        }
+    } else if (kernel_ms) {
         // per-kernel CUDA events around the step kernel on the engine stream
         std::vector<cudaEvent_t> ev(2 * steps);
         for (auto& x : ev) CU(cudaEventCreate(&x));

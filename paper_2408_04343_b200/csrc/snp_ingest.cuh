@@ -173,7 +173,7 @@ __global__ void ingest_stages_kernel(long long n_tiles, const uint32_t* __restri
                 const uint32_t n = (uint32_t)min((long long)kSub, nd - dd);
                 const uint32_t rf = P.roff[d0 + dd], rl = P.roff[d0 + dd + n];
                 const uint32_t r_al = P.tiny ? (rf & ~3u) : (P.wide ? rf : (rf & ~1u));
-                const uint32_t fixed = kPayload + r16(n * 8ull) + r16(n * 4ull) + (P.rpn ? 0u : r16((n + 1) * 4ull));
+                const uint32_t fixed = kPayload + kP2Rules(P.rpn != 0);
                 uint32_t rb = r16((unsigned long long)(rl - r_al) * rw_size);
                 if (fixed + rb > kStageBytes) rb = 0;
                 StageDesc sd;

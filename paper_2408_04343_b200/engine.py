@@ -80,7 +80,7 @@ _REC_FLAGS = {
 _FMT_CODES = {Format.SPARSE: nat.SNP_FMT_SPARSE, Format.ELL: nat.SNP_FMT_ELL,
               Format.COMPRESSED: nat.SNP_FMT_COMPRESSED}
 _VARIANTS = {"auto": nat.SNP_VARIANT_AUTO, "pull": nat.SNP_VARIANT_PULL, "push": nat.SNP_VARIANT_PUSH,
-             "tiled": nat.SNP_VARIANT_TILED, "tiled2": nat.SNP_VARIANT_TILED2}
+             "tiled": nat.SNP_VARIANT_TILED, "tiled2": nat.SNP_VARIANT_TILED2, "small": nat.SNP_VARIANT_SMALL}
 
 
 @dataclass(frozen=True)

@@ -162,3 +162,18 @@ def multi_amount_system(q: int, pmax: int, seed: int | None = None):
     rules = snp.RuleVector(threshold, r.is_exact, consumed, produced, r.delay, r.neuron)
     initial = base.initial + rng.integers(0, 3 * pmax, size=base.neuron_count)
     return snp.SystemArrays(initial, rules, base.rule_map, base.adj_offsets, base.adj_targets)
+
+
+def concentrated_system(q: int, hot: int = 256, deg: int = 16, seed: int = 5):
+    """synth-v1 rules (with delays) whose out-edges all land in the first `hot`
+    neurons: every delivery goes to one destination tile, so the binned push
+    overflows its shared-memory buckets on every step."""
+    import paper_2408_04343_b200 as snp
+    base = snp.synth_v1(q, with_delays=True)
+    rng = np.random.default_rng(seed)
+    key = rng.random((q, hot))
+    key[np.arange(hot), np.arange(hot)] = 2.0  # neurons in the hot set never pick themselves
+    tg = np.argsort(key, axis=1)[:, :deg].astype(np.int64)
+    tg.sort(axis=1)
+    adj_off = np.arange(0, deg * q + 1, deg, dtype=np.int64)
+    return snp.SystemArrays(base.initial, base.rules, base.rule_map, adj_off, tg.reshape(-1))

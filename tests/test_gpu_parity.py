@@ -17,8 +17,8 @@ from oracle.snp_oracle import OracleSystem, trace_digest
 pytestmark = pytest.mark.gpu
 
 FORMATS = [(snp.Format.SPARSE, "auto"), (snp.Format.ELL, "auto"), (snp.Format.COMPRESSED, "tiled"),
-           (snp.Format.COMPRESSED, "pull"), (snp.Format.COMPRESSED, "push")]
-FMT_IDS = ["sparse", "ell", "compressed-tiled", "compressed-pull", "compressed-push"]
+           (snp.Format.COMPRESSED, "pull"), (snp.Format.COMPRESSED, "push"), (snp.Format.COMPRESSED, "small")]
+FMT_IDS = ["sparse", "ell", "compressed-tiled", "compressed-pull", "compressed-push", "compressed-small"]
 POLICIES = {"first": snp.FirstApplicable(), "seeded7": snp.SeededRandom(7),
             "seeded_big": snp.SeededRandom(2**63 + 5)}
 
@@ -154,9 +154,11 @@ def test_sort2048_ell_sparse_to_halt(fmt):
     res = snp.run_final(prep, snp.SimOptions(max_steps=5 * n))
     assert res.halt_reason is snp.HaltReason.NO_APPLICABLE_RULES
     assert res.config[2 * n:].tolist() == sorted(values)
-    ref, want_c, _ = coracle.run(OracleSystem.from_arrays(a), 5 * n, 0, 0, trace_rows=31)
-    assert res.steps == ref.n_steps
+    full, want_c, _ = coracle.run(OracleSystem.from_arrays(a), 5 * n, 0, 0)
+    assert res.steps == full.n_steps
     np.testing.assert_array_equal(res.config, want_c)
+    # a 30-step run has 31 config rows but 30 spiking rows
+    ref, _, _ = coracle.run(OracleSystem.from_arrays(a), 30, 0, 0, trace_rows=31)
     mine = snp.simulate_prepared(prep, snp.SimOptions(max_steps=30, record=snp.RecordLevel.FULL))
     assert trace_digest(mine.configs, mine.delays, mine.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
     del prep
@@ -571,3 +573,19 @@ def test_push_step_kernels_match_oracle(mode, pmax, monkeypatch):
                                                         record=snp.RecordLevel.FULL))
         assert trace_digest(tr.configs, tr.delays, tr.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
         del prep
+
+
+@pytest.mark.parametrize("fmt,var", [(snp.Format.ELL, "auto"), (snp.Format.COMPRESSED, "push")], ids=["ell", "push"])
+def test_binned_push_bucket_overflow(fmt, var):
+    """Every delivery into one destination tile (50K sources x 16 targets in
+    256 neurons): the binned push's shared-memory buckets overflow into the
+    tile's overflow region on every step; 12 steps vs the C oracle."""
+    from conftest import concentrated_system
+    a = concentrated_system(50_000)
+    osys = OracleSystem.from_arrays(a)
+    _, want_c, want_d = coracle.run(osys, 12, 1, 4)
+    prep = snp.prepare(a, fmt, variant=var)
+    assert snp._native.PUSH_KERNELS[prep.engine.info["push_kernel"]] == "binned"
+    res = snp.run_final(prep, snp.SimOptions(max_steps=12, selection=snp.SeededRandom(4)))
+    np.testing.assert_array_equal(res.config, want_c)
+    np.testing.assert_array_equal(res.delays, want_d)

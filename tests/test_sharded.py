@@ -495,3 +495,60 @@ def test_sharded_negative_spikes_reported(world, exchange, extra):
                 break
             assert k < max_steps + 5
         assert halts[0] == want, (max_steps, halts)
+
+
+# -- GPU: the NCCL all-gather exchange itself (torch_allgather_exchange) -------------------
+
+def _nccl_worker(port, out):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        res = {}
+        for case in ("synth_delays", "sort"):
+            if case == "sort":
+                arrays, L = snp.sort_arrays(snp.SortInstance(200)), 300
+            else:
+                arrays, L = snp.synth_v1(40_000, with_delays=True), 9
+            q = arrays.neuron_count
+            lay = shd.shard_layout(q, 1)
+            sh = shd.ShardedEngine(shd.local_arrays(arrays, lay, 0), q, 0, 1, p_span=shd.p_range(arrays.rules))
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                ex = shd.torch_allgather_exchange(sh)
+                cfg, dly, steps, reason, _, launches = sh.run(L, exchange=ex)
+            res[case] = (cfg.tolist(), dly.tolist(), steps, str(reason), launches)
+        out.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_allgather_exchange_runs():
+    """The all-gather fallback through a real NCCL communicator (one rank:
+    NCCL refuses two ranks on one GPU, and the test box has one), with the
+    collective on the engine's stream after every launch -- the same code
+    path bench.py --gpus N takes with SNPB200_EXCHANGE=nccl."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(port, out))
+    p.start()
+    res = out.get(timeout=600)
+    p.join(60)
+    assert p.exitcode == 0
+    for case, (cfg, dly, steps, reason, launches) in res.items():
+        if case == "sort":
+            arrays, L = snp.sort_arrays(snp.SortInstance(200)), 300
+        else:
+            arrays, L = snp.synth_v1(40_000, with_delays=True), 9
+        want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED), snp.SimOptions(max_steps=L))
+        assert cfg == want.config.tolist() and dly == want.delays.tolist(), case
+        assert steps == want.steps and reason == str(want.halt_reason), case
+        assert launches >= steps

@@ -28,7 +28,7 @@ import paper_2408_04343_b200 as snp  # noqa: E402
 from bench import algorithmic_bytes, measured_peaks  # noqa: E402
 
 FORMATS = [("sparse", "auto"), ("ell", "auto"), ("compressed", "tiled"), ("compressed", "pull"),
-           ("compressed", "push")]
+           ("compressed", "push"), ("compressed", "small")]
 
 
 def fits(fmt: str, n: int) -> bool:
@@ -39,6 +39,10 @@ def fits(fmt: str, n: int) -> bool:
     if fmt == "ell":
         return m * (n + 2) * 8 < 120e9
     return True
+
+
+def fits_variant(variant: str, n: int) -> bool:
+    return variant != "small" or 3 * n <= 16384
 
 
 def measure(arrays, fmt: str, variant: str, steps: int, warmup: int = 3) -> dict:
@@ -80,7 +84,7 @@ def main():
     for n in [int(x) for x in a.sizes.split(",") if x]:
         arrays = snp.sort_arrays(snp.SortInstance(n))
         for fmt, var in FORMATS:
-            if not fits(fmt, n):
+            if not fits(fmt, n) or not fits_variant(var, n):
                 continue
             r = measure(arrays, fmt, var, n + 1)
             r.update({"workload": f"sort n={n}", "q": arrays.neuron_count, "m": arrays.rule_count,

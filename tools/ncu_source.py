@@ -15,7 +15,7 @@ import io
 import subprocess
 
 
-def load(report: str, view: str = "cuda") -> list[dict]:
+def load(report: str, view: str = "cuda,sass") -> list[dict]:
     out = subprocess.run(["ncu", "-i", report, "--page", "source", "--csv", "--print-source", view],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -26,10 +26,19 @@ def load(report: str, view: str = "cuda") -> list[dict]:
         if len(r) == 1 and r[0].strip():
             fname = r[0].strip()  # some ncu versions print the file path on its own line
             continue
-        if hdr is None or r[0] in ("#", "Line", "# Address", "Address"):
+        if r[0] in ("File Path", "File Name") and len(r) == 2:
+            fname = r[1].strip()  # ncu 2025: a ("File Path", path) row per file
+            continue
+        if r[0] == "Function Name":
+            continue
+        if hdr is None or r[0] in ("#", "Line", "Line No", "# Address", "Address"):
             hdr = r
             continue
-        d = dict(zip(hdr, r))
+        if view == "cuda,sass" and not r[0]:
+            continue  # the mixed view's SASS rows under each source line
+        d = {}
+        for h_, v_ in zip(hdr, r):
+            d.setdefault(h_, v_)  # the first "Source" column is the CUDA line
         d["_file"] = fname
         res.append(d)
     return res
@@ -66,7 +75,7 @@ def main():
     for d in rows:
         if a.file and d.get("_file") and a.file not in d["_file"]:
             continue
-        ln = pick(d, "#", "Line", "Line Number")
+        ln = pick(d, "Line No", "#", "Line", "Line Number")
         inst = num(pick(d, "Instructions Executed", "inst_executed"))
         stall = num(pick(d, "Warp Stall Sampling (All Samples)", "Warp Stall Sampling"))
         src = pick(d, "Source") or ""
