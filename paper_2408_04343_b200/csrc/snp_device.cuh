@@ -29,6 +29,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace snp {
@@ -124,6 +125,10 @@ struct DevSys {
     const uint2* hx_e;
     const uint32_t* hx_aoff;
     const uint2* hx_a;
+    // dense FirstApplicable table per heavy neuron (null / empty range = none):
+    // hx_lut[hx_loff[h] + min(C, len - 1)] = local rule index or ~0
+    const uint32_t* hx_loff;
+    const uint32_t* hx_lut;
     int light_ctas;           // CTAs striding over light tiles
     int heavy_ctas;           // CTAs striding over the heavy list
     long long light_tiles;    // ceil(q / 256)
@@ -142,7 +147,7 @@ struct DevSys {
     int ring;                   // TMA ring stages (<= kMaxRing)
     int rpn;                    // tiled: rules per neuron when every neuron has the same count (<= 32), else 0
     int pf;                     // tiled: ring stages prefetched into L2 ahead of the TMA copies (0 = off)
-    int dbg;                    // timing experiments (SNPB200_DEBUG_SKIP): 1 skip phase-1 math, 2 skip phase 2
+    int dbg;                    // timing experiments (SNPB200_DEBUG_SKIP): 1 skip phase-1 math, 2 skip phase 2, 4 generic phase-2 loop
     long long n_tiles;
     // row partition (sharded.py): local neuron j is global neuron gbase + j and
     // publishes its P element (bit / u8 / u16 / u32) at exchange-space
@@ -660,6 +665,14 @@ __device__ __forceinline__ uint32_t warp_bound(const uint2* __restrict__ keys, u
 // heavy_first_applicable, one warp (all lanes get the answer).
 __device__ __forceinline__ int heavy_first_applicable_warp(const DevSys& s, int h, long long C, int lane) {
     if (C < 0) return -1;
+    if (s.hx_loff) {
+        const uint32_t l0 = __ldg(s.hx_loff + h), l1 = __ldg(s.hx_loff + h + 1);
+        if (l1 > l0) {
+            const uint32_t c = C >= (long long)(l1 - l0 - 1) ? l1 - l0 - 1 : (uint32_t)C;
+            const uint32_t v = __ldg(s.hx_lut + l0 + c);
+            return v == 0xffffffffu ? -1 : (int)v;
+        }
+    }
     const uint32_t cc = (C >> 31) != 0 ? 0x80000000u : (uint32_t)C;
     uint32_t best = 0xffffffffu;
     {   // exactly: the first threshold >= cc, if it equals cc
@@ -1291,12 +1304,20 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
         // rank saw a negative count when finishing step k-2
         const bool last = k - 1 >= vc->max_steps;
         if (n || last || (!f && !c)) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
-                ctl->halted = 1;
-                ctl->reason = n ? HALT_NEGATIVE : (last ? HALT_STEP_LIMIT : HALT_NO_APPLICABLE);
-                if (!n) ctl->step = k - 1;
-                ctl->neg_any = n ? 1 : 0;
-                ctl->push_armed = 0;
+            // the LAST CTA to get here publishes the halt: a CTA of this grid
+            // that starts late reads Ctrl.halted / Ctrl.step at its top, so an
+            // early writer could hand it step k-1 and a stray step
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1) {
+                    ctl->halted = 1;
+                    ctl->reason = n ? HALT_NEGATIVE : (last ? HALT_STEP_LIMIT : HALT_NO_APPLICABLE);
+                    if (!n) ctl->step = k - 1;
+                    ctl->neg_any = n ? 1 : 0;
+                    ctl->push_armed = 0;
+                    ctl->blocks_done = 0;
+                    __threadfence();
+                }
             }
             return;
         }
@@ -1570,7 +1591,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
             consumer_sync(kTileThreads);  // acc complete
 
             // ---- phase 2: finish step k-1, select step k (one destination per thread)
-            if (LEAN && TINY && kP2Rep == 1 && s.rpn > 0 && s.rpn <= 4 && (s.dbg & 2) == 0) {
+            if (LEAN && TINY && kP2Rep == 1 && s.rpn > 0 && s.rpn <= 4 && (s.dbg & 6) == 0) {
                 // Regular systems with <= 4 rules per neuron (implicit offsets,
                 // no heavy neurons): the stage addresses are constants and the
                 // per-stage bookkeeping is a header load, the wait and one
@@ -2492,10 +2513,13 @@ constexpr int kSmallThreads = 1024;
 constexpr long long kSmallMaxQ = 16384;   // 128 KB of int64 receive counters
 
 #ifndef SNP_TEMPLATES_ONLY
-template <bool WIDE>
+// R64: 64-bit receive counters (some destination can receive >= 2^31 in one
+// step); else 32-bit, whose shared-memory atomics are native
+template <bool WIDE, bool R64>
 __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __grid_constant__ DevSys s, DevState st) {
+    using RT = typename std::conditional<R64, unsigned long long, unsigned int>::type;
     extern __shared__ __align__(128) uint8_t smem[];
-    long long* recv_s = reinterpret_cast<long long*>(smem);  // [q] deliveries of the previous step
+    RT* recv_s = reinterpret_cast<RT*>(smem);  // [q] deliveries of the previous step
     __shared__ long long sh_neg_idx, sh_neg_val;
     __shared__ int sh_go;
     Ctrl* ctl = st.ctrl;
@@ -2512,7 +2536,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
     const bool stats_on = vc->stats_on != 0;
     const unsigned long long seed = vc->seed;
     long long k = vc->step;
-    for (long long j = threadIdx.x; j < q; j += kSmallThreads) recv_s[j] = st.recv[j];
+    for (long long j = threadIdx.x; j < q; j += kSmallThreads) recv_s[j] = (RT)st.recv[j];
     __syncthreads();
     for (;;) {
         const bool sel = k < max_steps;
@@ -2528,7 +2552,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
             const int dsv = st.ds[j];
             const int D = ds_next(dsv);
             long long C = st.cfg[j];
-            const long long rv = recv_s[j];
+            const long long rv = R64 ? (long long)recv_s[j] : (long long)(int)recv_s[j];
             recv_s[j] = 0;
             if (ds_open(dsv)) C += rv;
             if (nr > kLightRules) {
@@ -2601,17 +2625,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
             }
         }
         __syncthreads();
-        // ---- C
+        // ---- C (one warp per fired neuron, lanes over its out-edges)
         if (sel) {
-            for (long long j = threadIdx.x; j < q; j += kSmallThreads) {
+            for (long long j = warp; j < q; j += kSmallThreads / 32) {
                 const int r = st.chosen[j];
                 if (r < 0) continue;
-                const long long p = __ldg(&s.rrec[r].y);
+                const int p = __ldg(&s.rrec[r].y);
                 if (p <= 0) continue;
                 const uint32_t e0 = __ldg(s.soff + j), e1 = __ldg(s.soff + j + 1);
-                stat[ST_EDGES] += e1 - e0;
-                for (uint32_t e = e0; e < e1; ++e)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(recv_s + __ldg(s.sdst + e)), (unsigned long long)p);
+                if (lane == 0) stat[ST_EDGES] += e1 - e0;
+                for (uint32_t e = e0 + lane; e < e1; e += 32) atomicAdd(recv_s + __ldg(s.sdst + e), (RT)p);
             }
         }
         // ---- D
@@ -2653,7 +2676,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
         if (!sh_go) break;
         ++k;
     }
-    for (long long j = threadIdx.x; j < q; j += kSmallThreads) st.recv[j] = recv_s[j];
+    for (long long j = threadIdx.x; j < q; j += kSmallThreads)
+        st.recv[j] = R64 ? (long long)recv_s[j] : (long long)(int)recv_s[j];
     __threadfence();
 }
 #endif  // SNP_TEMPLATES_ONLY

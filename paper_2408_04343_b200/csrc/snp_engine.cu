@@ -803,7 +803,9 @@ struct PhaseTimer {
 int allow_max_smem(const void* fn, int device) {
     int optin = 0;
     CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    cudaFuncAttributes fa;
+    CU(cudaFuncGetAttributes(&fa, fn));
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
     return SNP_OK;
 }
 
@@ -1171,6 +1173,41 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             eoff[h + 1] = (uint32_t)ev.size();
             aoff[h + 1] = (uint32_t)av.size();
         }
+        // dense table over the count when a neuron's thresholds are compact
+        // (max threshold <= 4 x its rules + 64): entry c = the FirstApplicable
+        // rule for count c, the last entry for every count above the largest
+        // threshold -- one dependent load instead of two 32-ary searches
+        std::vector<uint32_t> loff(heavy.size() + 1, 0), lut;
+        for (size_t h = 0; h < heavy.size(); ++h) {
+            const uint32_t i = heavy[h], a = roff[i], b = roff[i + 1];
+            uint32_t mt = 0;
+            for (uint32_t r = a; r < b; ++r) mt = std::max(mt, rthr[r] & ~kExactBit);
+            const unsigned long long need = (unsigned long long)mt + 2;
+            if (mt > 4ull * (b - a) + 64 || lut.size() + need > (1ull << 28)) {
+                loff[h + 1] = (uint32_t)lut.size();  // no table: the guard index
+                continue;
+            }
+            std::vector<uint32_t> exf(mt + 2, 0xffffffffu), alf(mt + 2, 0xffffffffu);
+            for (uint32_t r = a; r < b; ++r) {
+                const uint32_t t = rthr[r] & ~kExactBit;
+                uint32_t& slot = (rthr[r] & kExactBit) ? exf[t] : alf[t];
+                slot = std::min(slot, r - a);
+            }
+            uint32_t best_al = 0xffffffffu;
+            for (uint32_t c = 0; c <= mt; ++c) {
+                best_al = std::min(best_al, alf[c]);
+                lut.push_back(std::min(best_al, exf[c]));
+            }
+            lut.push_back(best_al);  // counts above every threshold: at-least rules only
+            loff[h + 1] = (uint32_t)lut.size();
+        }
+        if (!lut.empty()) {
+            uint32_t *d_loff, *d_lut;
+            TRY(upload(e, &d_loff, loff));
+            TRY(upload(e, &d_lut, lut));
+            s.hx_loff = d_loff;
+            s.hx_lut = d_lut;
+        }
         uint32_t *d_eoff, *d_aoff;
         uint2 *d_ev, *d_av;
         TRY(upload(e, &d_eoff, eoff));
@@ -1445,8 +1482,14 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     } else if (e->format == SNP_FMT_COMPRESSED) {
         pick_fns<RECV_ARRAY, P_BIT, true, false>(e->wide_rules, &e->step_fn, &e->prime_fn);
         if (e->variant == SNP_VARIANT_SMALL) {
-            e->small_fn = e->wide_rules ? small_run_kernel<true> : small_run_kernel<false>;
-            e->small_smem = (size_t)std::max<long long>(1, q) * 8;
+            // 32-bit receive counters unless a destination can get 2^31 in a step
+            std::vector<uint32_t> ind(std::max<long long>(1, q), 0);
+            uint32_t mx = 0;
+            for (uint32_t t : sdst) mx = std::max(mx, ++ind[t]);
+            const bool r64 = (double)mx * (double)std::max<long long>(1, pmax) >= 2147483648.0;
+            e->small_fn = e->wide_rules ? (r64 ? small_run_kernel<true, true> : small_run_kernel<true, false>)
+                                        : (r64 ? small_run_kernel<false, true> : small_run_kernel<false, false>);
+            e->small_smem = (size_t)std::max<long long>(1, q) * (r64 ? 8 : 4);
             TRY(allow_max_smem((const void*)e->small_fn, e->device));
         }
     } else if (e->format == SNP_FMT_ELL) {
