@@ -147,7 +147,7 @@ struct DevSys {
     int ring;                   // TMA ring stages (<= kMaxRing)
     int rpn;                    // tiled: rules per neuron when every neuron has the same count (<= 32), else 0
     int pf;                     // tiled: ring stages prefetched into L2 ahead of the TMA copies (0 = off)
-    int dbg;                    // timing experiments (SNPB200_DEBUG_SKIP): 1 skip phase-1 math, 2 skip phase 2, 4 generic phase-2 loop
+    int dbg;                    // timing experiments (SNPB200_DEBUG_SKIP): 1 skip phase-1 math, 2 skip phase 2
     long long n_tiles;
     // row partition (sharded.py): local neuron j is global neuron gbase + j and
     // publishes its P element (bit / u8 / u16 / u32) at exchange-space
@@ -185,6 +185,7 @@ struct DevSys {
     int bin_amount;                // UNIT entries: the common amount of every delivery
     const uint32_t* bin_off;       // [ntiles + 1] main region starts (entries, multiples of 8)
     const uint32_t* bin_ooff;      // [ntiles + 1] overflow region starts (same buffer, after the main regions)
+    int bin_cpc;                   // ELL: 16-byte chunks per column (ell_ld / 2) when <= 16, else 0
 };
 
 struct DevState {
@@ -1591,73 +1592,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
             consumer_sync(kTileThreads);  // acc complete
 
             // ---- phase 2: finish step k-1, select step k (one destination per thread)
-            if (LEAN && TINY && kP2Rep == 1 && s.rpn > 0 && s.rpn <= 4 && (s.dbg & 6) == 0) {
-                // Regular systems with <= 4 rules per neuron (implicit offsets,
-                // no heavy neurons): the stage addresses are constants and the
-                // per-stage bookkeeping is a header load, the wait and one
-                // arrival -- the generic loop below spends more instructions on
-                // that than on the selection itself (ncu source view, K3).
-                const uint32_t nr = (uint32_t)s.rpn;
-                const int li = threadIdx.x;
-                for (;;) {
-                    const int b = cb;
-                    const uint8_t* buf = ring + b * kStageBytes;
-                    mbar_wait(&full_bar[b], cround & 1u);
-                    if (++cb == nst) {
-                        cb = 0;
-                        ++cround;
-                    }
-                    const uint4 hd = *reinterpret_cast<const uint4*>(buf);      // kind, last, first, n
-                    const uint2 hr = *reinterpret_cast<const uint2*>(buf + 24);  // r_al, rstaged
-                    const uint32_t n = hd.w;
-                    const bool active = li < (int)n;
-                    const int i = (int)hd.z + li;
-                    const long long j = d0 + i;
-                    long long Cprev = 0;
-                    int dsv = 0;
-                    alignas(16) uint32_t wv[4] = {0u, 0u, 0u, 0u};
-                    if (active) {
-                        Cprev = reinterpret_cast<const long long*>(buf + kPayload)[li];
-                        dsv = reinterpret_cast<const int*>(buf + kPayload + kP2Ds)[li];
-                        const uint32_t r0 = nr * (uint32_t)j;
-                        if (hr.y) {
-                            const uint32_t* rp =
-                                reinterpret_cast<const uint32_t*>(buf + kPayload + kP2Rules(true)) + (r0 - hr.x);
-                            if (nr == 4) {
-                                const uint4 v = *reinterpret_cast<const uint4*>(rp);  // r_al = 4 * first neuron
-                                wv[0] = v.x, wv[1] = v.y, wv[2] = v.z, wv[3] = v.w;
-                            } else {
-#pragma unroll
-                                for (int x = 0; x < 4; ++x) wv[x] = rp[x];  // words past nr are masked off
-                            }
-                        } else {
-                            for (uint32_t x = 0; x < nr; ++x) wv[x] = __ldg(s.rw4 + r0 + x);
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty_bar[b]);
-                    long long pval = 0;
-                    if (active) {
-                        long long C = Cprev;
-                        if (ds_open(dsv)) {
-                            const uint32_t gsum = tile_acc_get<CB>(acc, i);
-                            C += (PM == P_BIT) ? (long long)gsum * s.p_common : (long long)gsum;
-                        }
-                        const int D = ds_next(dsv);
-                        pval = lean_commit4<PM, true>(s, st, ctl, cx, j, nr, wv, C, D, sel && D == 0, t_fired, t_closed,
-                                                      t_neg);
-                    }
-                    if (sel && PM == P_BIT) {
-                        const unsigned int bits = __ballot_sync(0xffffffffu, pval > 0);
-                        if (lane == 0 && warp * 32 < (int)n) {
-                            const long long wd = (j + s.xbase) >> 5;
-                            Pzero[wd] = 0u;
-                            Pcur[wd] = bits;
-                        }
-                    }
-                    if (hd.y) break;
-                }
-            } else for (;;) {
+            for (;;) {
                 const int b = cb;
                 const uint8_t* buf = ring + b * kStageBytes;
                 mbar_wait(&full_bar[b], cround & 1u);
@@ -2266,6 +2201,10 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
     const uint32_t acc_s = smem_u32(acc), cnt_s = smem_u32(cnt), stage_s = smem_u32(stage);
     const unsigned long long magic = s.bin_magic;
     const E pad = UNIT ? (E)T : (E)0;  // adds to the dummy counter / adds 0
+    // ELL column groups: cpc chunks per column, `per` columns per warp pass
+    __shared__ uint32_t col_r[kBinThreads / 32][32], col_l[kBinThreads / 32][32];
+    const uint32_t cpc = ELL ? (uint32_t)s.bin_cpc : 0u;
+    const uint32_t per = cpc ? 32u / cpc : 0u, sub = cpc ? (uint32_t)lane / cpc : 0u, cc = (uint32_t)lane - sub * cpc;
 
     unsigned int stat[ST_COUNT];
 #pragma unroll
@@ -2379,7 +2318,40 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
             };
             const uint32_t total = __reduce_add_sync(0xffffffffu, nch);
             const uint32_t mx = __reduce_max_sync(0xffffffffu, nch);
-            if (mx * 32u <= 2u * total) {
+            if (ELL && cpc) {
+                // column groups: the warp's fired columns, compacted in shared
+                // memory, `per` at a time; lane sub * cpc + cc reads chunk cc of
+                // column sub, so each column is one contiguous 16 * cpc-byte read
+                const uint32_t fm = __ballot_sync(0xffffffffu, nch > 0);
+                const uint32_t nf = __popc(fm);
+                if (nch > 0) {
+                    const uint32_t rank = __popc(fm & ((1u << lane) - 1u));
+                    col_r[warp][rank] = (uint32_t)r;
+                    col_l[warp][rank] = len;
+                }
+                __syncwarp();
+                for (uint32_t i0 = 0; i0 < nf; i0 += per * kBinUnroll) {
+                    int4 v[kBinUnroll];
+                    uint32_t L[kBinUnroll];
+#pragma unroll
+                    for (int u = 0; u < kBinUnroll; ++u) {
+                        const uint32_t col = i0 + u * per + sub;
+                        v[u] = make_int4(-1, 0, -1, 0);
+                        L[u] = 0;
+                        if (sub < per && col < nf) {
+                            L[u] = col_l[warp][col];
+                            if (2 * cc < L[u]) v[u] = ld_stream16(s.ell + (long long)col_r[warp][col] * s.ell_ld + 2 * cc, pol);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBinUnroll; ++u) {
+                        if (2 * cc >= L[u]) continue;
+                        if (cc > 0) deliver((uint32_t)v[u].x, (uint32_t)v[u].y);  // row 0 = consumption
+                        if (2 * cc + 1 < L[u]) deliver((uint32_t)v[u].z, (uint32_t)v[u].w);
+                    }
+                }
+                __syncwarp();
+            } else if (mx * 32u <= 2u * total) {
                 // lane-own columns: lane l walks its column, kBinUnroll chunks in flight
                 for (uint32_t cb0 = 0; cb0 < mx; cb0 += kBinUnroll) {
                     int4 v[kBinUnroll];
@@ -2387,9 +2359,9 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
                     for (int u = 0; u < kBinUnroll; ++u) {
                         const uint32_t c = cb0 + u;
                         v[u] = make_int4(-1, 0, -1, 0);
-                        if (c < nch) {
-                            if (ELL) v[u] = ld_stream16(s.ell + base + 2 * c, pol);
-                            else v[u].x = (int)ld_stream4(s.sdst + base + c, pol);
+                        if (c < nch) {  // L1-allocating: the lane reads the rest of the sector next
+                            if (ELL) v[u] = __ldg(reinterpret_cast<const int4*>(s.ell + base + 2 * c));
+                            else v[u].x = (int)__ldg(s.sdst + base + c);
                         }
                     }
 #pragma unroll

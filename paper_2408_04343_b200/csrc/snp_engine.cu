@@ -1383,6 +1383,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                 s.bin_magic = (~0ull / (unsigned long long)T) + 1ull;
                 s.bin_amount = unit ? (int)amin : 1;
                 s.bin_off = d_boff;
+                s.bin_cpc = (e->format == SNP_FMT_ELL && ell_ld / 2 <= 16) ? (int)(ell_ld / 2) : 0;
                 e->bin_cb = cb;
                 e->bin_unit = unit;
                 e->bin_smem = smem;

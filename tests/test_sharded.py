@@ -430,8 +430,8 @@ def test_peer_exchange_tiled2_matches_single(world, monkeypatch):
     want = snp.run_final(snp.prepare(arrays, snp.Format.COMPRESSED), snp.SimOptions(max_steps=10, selection=sel))
     orig = shd.ShardedEngine.__init__
 
-    def init_tiled2(self, local, q, rank, world, device=0, variant="tiled"):
-        orig(self, local, q, rank, world, device, variant="tiled2")
+    def init_tiled2(self, local, q, rank, world, device=0, variant="tiled", p_span=None):
+        orig(self, local, q, rank, world, device, variant="tiled2", p_span=p_span)
 
     monkeypatch.setattr(shd.ShardedEngine, "__init__", init_tiled2)
     cfg, dly, steps, _ = _run_p2p_on_one_gpu(arrays, world, 10, sel)
