@@ -1271,6 +1271,11 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
     __shared__ __align__(16) StageDesc desc_s[32];
     Ctrl* ctl = st.ctrl;
     const volatile Ctrl* vc = ctl;
+    // launched with programmatic stream serialization: wait for the previous
+    // step's grid to complete (and its writes to be visible) before reading
+    // anything it wrote; the next step's grid may be scheduled right away
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int halted = vc->halted;
     const long long k = vc->step;
     if (halted || k >= vc->stop_at) {
@@ -2128,7 +2133,7 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const
 //   A. receive: the tile's bin entries written during step k-1 (main region:
 //      whole 16-byte units; overflow region: single entries) -> 8/16/32-bit
 //      counters in shared memory;
-//   B. for 1024 destinations at a time: finish step k-1 (C += open ? recv),
+//   B. for kBinThreads destinations at a time: finish step k-1 (C += open ? recv),
 //      update delays, select step k (sv_calc), consume (row 0 of the ELL
 //      column, applied at selection like COMPRESSED);
 //   C. walk the fired neurons' columns (ELL rows 1.., 16-byte loads with an
@@ -2147,7 +2152,11 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const
 // them.  Region sizes: main = the tile's in-degree sum + the padding of every
 // possible flush, overflow = the in-degree sum (checked on every reservation).
 
-constexpr int kBinThreads = 1024;
+#ifndef SNP_BIN_THREADS
+#define SNP_BIN_THREADS 768  // 24 warps: 80 registers per thread (1024 threads leave 64, and the
+                             // delivery loop then rematerialises per-kernel constants -- ncu source view)
+#endif
+constexpr int kBinThreads = SNP_BIN_THREADS;
 constexpr int kBinUnroll = 4;    // column chunks in flight per lane
 
 template <bool UNIT>
@@ -2160,17 +2169,22 @@ struct BinEntry {
 template <>
 struct BinEntry<true> {
     using T = uint16_t;
-    static constexpr int kCap = 128;
-    static constexpr int kWin = 2;
+    static constexpr int kCap = 256;
+    static constexpr int kWin = 4;
     static constexpr int kVec = 8;
 };
 // flushes per step into one tile are at most ceil(q / (kBinThreads * kWin)) + ntiles
-__host__ __device__ constexpr long long bin_flush_dests(bool unit) { return unit ? 2048 : 1024; }
+__host__ __device__ constexpr long long bin_flush_dests(bool unit) {
+    return (long long)kBinThreads * (unit ? BinEntry<true>::kWin : BinEntry<false>::kWin);
+}
 
 template <int CB>
 __host__ __device__ constexpr int bin_acc_words(int T) { return (acc_words<CB>(T) + 3) & ~3; }
 
-template <bool ELL, bool WIDE, bool UNIT, int CB>
+// GROUP: ELL column-group walk only (uniform column stride <= 16 chunks);
+// else lane-own / concatenated walks -- separate instances keep the register
+// budget of each (1024 threads: 64 registers) for its own path
+template <bool ELL, bool WIDE, bool UNIT, int CB, bool GROUP>
 __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __grid_constant__ DevSys s, DevState st) {
     using BE = BinEntry<UNIT>;
     using E = typename BE::T;
@@ -2202,8 +2216,8 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
     const unsigned long long magic = s.bin_magic;
     const E pad = UNIT ? (E)T : (E)0;  // adds to the dummy counter / adds 0
     // ELL column groups: cpc chunks per column, `per` columns per warp pass
-    __shared__ uint32_t col_r[kBinThreads / 32][32], col_l[kBinThreads / 32][32];
-    const uint32_t cpc = ELL ? (uint32_t)s.bin_cpc : 0u;
+    __shared__ uint32_t col_r[kBinThreads / 32][32];
+    const uint32_t cpc = (ELL && GROUP) ? (uint32_t)s.bin_cpc : 0u;
     const uint32_t per = cpc ? 32u / cpc : 0u, sub = cpc ? (uint32_t)lane / cpc : 0u, cc = (uint32_t)lane - sub * cpc;
 
     unsigned int stat[ST_COUNT];
@@ -2250,7 +2264,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
             fill_in[tile] = 0;
             fill_in[NT + tile] = 0;
         }
-        // ---- B + C (+ D every kWin chunks), 1024 destinations at a time
+        // ---- B + C (+ D every kWin chunks), kBinThreads destinations at a time
         for (int c0 = 0, win = 0; c0 < nd; c0 += kBinThreads, ++win) {
             const int li = c0 + threadIdx.x;
             const long long j = d0 + li;
@@ -2284,7 +2298,11 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
             // consumption, already applied; Optimized: one target per lane)
             uint32_t nch = 0, len = 0;
             long long base = 0;
-            if (sel && r >= 0) {
+            if (GROUP) {
+                // column groups read whole padded columns (padding pairs have
+                // target -1), so the per-rule length array is not read
+                nch = (sel && r >= 0) ? 1u : 0u;
+            } else if (sel && r >= 0) {
                 if (ELL) {
                     len = __ldg(s.ell_len + r);
                     nch = len > 1 ? (len + 1) >> 1 : 0u;
@@ -2318,40 +2336,33 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
             };
             const uint32_t total = __reduce_add_sync(0xffffffffu, nch);
             const uint32_t mx = __reduce_max_sync(0xffffffffu, nch);
-            if (ELL && cpc) {
+            if constexpr (ELL && GROUP) {
                 // column groups: the warp's fired columns, compacted in shared
                 // memory, `per` at a time; lane sub * cpc + cc reads chunk cc of
                 // column sub, so each column is one contiguous 16 * cpc-byte read
                 const uint32_t fm = __ballot_sync(0xffffffffu, nch > 0);
                 const uint32_t nf = __popc(fm);
-                if (nch > 0) {
-                    const uint32_t rank = __popc(fm & ((1u << lane) - 1u));
-                    col_r[warp][rank] = (uint32_t)r;
-                    col_l[warp][rank] = len;
-                }
+                if (nch > 0) col_r[warp][__popc(fm & ((1u << lane) - 1u))] = (uint32_t)r;
                 __syncwarp();
                 for (uint32_t i0 = 0; i0 < nf; i0 += per * kBinUnroll) {
                     int4 v[kBinUnroll];
-                    uint32_t L[kBinUnroll];
 #pragma unroll
                     for (int u = 0; u < kBinUnroll; ++u) {
                         const uint32_t col = i0 + u * per + sub;
                         v[u] = make_int4(-1, 0, -1, 0);
-                        L[u] = 0;
-                        if (sub < per && col < nf) {
-                            L[u] = col_l[warp][col];
-                            if (2 * cc < L[u]) v[u] = ld_stream16(s.ell + (long long)col_r[warp][col] * s.ell_ld + 2 * cc, pol);
-                        }
+                        if (sub < per && col < nf)
+                            v[u] = ld_stream16(s.ell + (long long)col_r[warp][col] * s.ell_ld + 2 * cc, pol);
                     }
 #pragma unroll
                     for (int u = 0; u < kBinUnroll; ++u) {
-                        if (2 * cc >= L[u]) continue;
-                        if (cc > 0) deliver((uint32_t)v[u].x, (uint32_t)v[u].y);  // row 0 = consumption
-                        if (2 * cc + 1 < L[u]) deliver((uint32_t)v[u].z, (uint32_t)v[u].w);
+                        if (cc > 0 && v[u].x >= 0) deliver((uint32_t)v[u].x, (uint32_t)v[u].y);  // row 0 = consumption
+                        if (v[u].z >= 0) deliver((uint32_t)v[u].z, (uint32_t)v[u].w);
+                        edges += (cc > 0 && v[u].x >= 0 ? 1u : 0u) + (v[u].z >= 0 ? 1u : 0u);
                     }
                 }
                 __syncwarp();
-            } else if (mx * 32u <= 2u * total) {
+            } else {
+            if (mx * 32u <= 2u * total) {
                 // lane-own columns: lane l walks its column, kBinUnroll chunks in flight
                 for (uint32_t cb0 = 0; cb0 < mx; cb0 += kBinUnroll) {
                     int4 v[kBinUnroll];
@@ -2420,6 +2431,7 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
                     }
                 }
             }
+            }  // GROUP
             if ((win + 1) % kWin != 0 && c0 + kBinThreads < nd) continue;  // keep staging
             __syncthreads();
             // ---- D. flush every bucket: pad to whole 16-byte units, one reservation, vector stores

@@ -142,6 +142,7 @@ struct snp_engine {
     size_t bin_smem = 0;       // binned push: dynamic shared memory
     PrimeFn prime_fn = nullptr;
     StepFn small_fn = nullptr;  // variant SMALL: one-CTA loop-segment kernel for runs
+    bool pdl = true;            // tiled: programmatic dependent launch (SNPB200_PDL=0: off)
     size_t small_smem = 0;
     int step_grid = 0;
     int push_grid = 0;
@@ -362,6 +363,7 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint3
     if (const char* env = getenv("SNPB200_PREFETCH")) s.pf = std::max(0, atoi(env));
     s.dbg = 0;
     if (const char* env = getenv("SNPB200_DEBUG_SKIP")) s.dbg = atoi(env);
+    if (const char* env = getenv("SNPB200_PDL")) e->pdl = atoi(env) != 0;
     // regular rule counts: offsets are implicit (rpn * local neuron)
     s.rpn = 0;
     if (q > 0) {
@@ -778,9 +780,29 @@ StepFn run_fn(const snp_engine* e) {
 
 // The step kernel of a run (the one-kernel push step when the engine has one).
 void launch_main(snp_engine* e) {
-    if (e->small_fn) e->small_fn<<<1, kSmallThreads, e->small_smem, e->stream>>>(e->sys, e->st);
-    else if (e->fused_fn) e->fused_fn<<<e->fused_grid, e->fused_block, e->fused_smem, e->stream>>>(e->sys, e->st);
-    else run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
+    if (e->small_fn) {
+        e->small_fn<<<1, kSmallThreads, e->small_smem, e->stream>>>(e->sys, e->st);
+    } else if (e->fused_fn) {
+        e->fused_fn<<<e->fused_grid, e->fused_block, e->fused_smem, e->stream>>>(e->sys, e->st);
+    } else if (e->tiled && e->pdl) {
+        // programmatic dependent launch: the step kernel's CTAs are scheduled
+        // while the previous step's grid drains and wait in griddepcontrol.wait
+        // (full completion + visibility of the previous grid) -- hides the
+        // launch gap between consecutive steps
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(e->step_grid);
+        cfg.blockDim = dim3(e->step_block);
+        cfg.dynamicSmemBytes = e->step_smem;
+        cfg.stream = e->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, run_fn(e), e->sys, e->st);
+    } else {
+        run_fn(e)<<<e->step_grid, e->step_block, e->step_smem, e->stream>>>(e->sys, e->st);
+    }
 }
 
 // SNPB200_TIMING=1: per-phase host timings of engine creation on stderr
@@ -1388,13 +1410,16 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                 e->bin_unit = unit;
                 e->bin_smem = smem;
                 const bool ell = e->format == SNP_FMT_ELL, w = e->wide_rules;
-#define SNP_BIN_PICK(E_, W_, U_)                                                                    \
-    (cb == 8 ? ell_bin_step_kernel<E_, W_, U_, 8> : (cb == 16 ? ell_bin_step_kernel<E_, W_, U_, 16>  \
-                                                              : ell_bin_step_kernel<E_, W_, U_, 32>))
-                if (ell) e->fused_fn = w ? (unit ? SNP_BIN_PICK(true, true, true) : SNP_BIN_PICK(true, true, false))
-                                         : (unit ? SNP_BIN_PICK(true, false, true) : SNP_BIN_PICK(true, false, false));
-                else e->fused_fn = w ? (unit ? SNP_BIN_PICK(false, true, true) : SNP_BIN_PICK(false, true, false))
-                                     : (unit ? SNP_BIN_PICK(false, false, true) : SNP_BIN_PICK(false, false, false));
+                const bool grp = s.bin_cpc > 0;
+#define SNP_BIN_PICK(E_, W_, U_, G_)                                                                      \
+    (cb == 8 ? ell_bin_step_kernel<E_, W_, U_, 8, G_> : (cb == 16 ? ell_bin_step_kernel<E_, W_, U_, 16, G_>  \
+                                                                  : ell_bin_step_kernel<E_, W_, U_, 32, G_>))
+#define SNP_BIN_PICK_G(W_, U_) (grp ? SNP_BIN_PICK(true, W_, U_, true) : SNP_BIN_PICK(true, W_, U_, false))
+                if (ell) e->fused_fn = w ? (unit ? SNP_BIN_PICK_G(true, true) : SNP_BIN_PICK_G(true, false))
+                                         : (unit ? SNP_BIN_PICK_G(false, true) : SNP_BIN_PICK_G(false, false));
+                else e->fused_fn = w ? (unit ? SNP_BIN_PICK(false, true, true, false) : SNP_BIN_PICK(false, true, false, false))
+                                     : (unit ? SNP_BIN_PICK(false, false, true, false) : SNP_BIN_PICK(false, false, false, false));
+#undef SNP_BIN_PICK_G
 #undef SNP_BIN_PICK
                 TRY(allow_max_smem((const void*)e->fused_fn, e->device));
             }

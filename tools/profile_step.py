@@ -14,8 +14,11 @@ p.add_argument("--variant", default="tiled")
 p.add_argument("--policy", default="first")
 p.add_argument("--steps", type=int, default=6)
 p.add_argument("--q", type=int, default=10_000_000)
+p.add_argument("--sort", type=int, default=0, help="sort instance n (workload ignored)")
 a = p.parse_args()
-if a.workload == "k2":
+if a.sort:
+    arrays = snp.sort_arrays(snp.SortInstance(a.sort))
+elif a.workload == "k2":
     arrays = snp.sort_arrays(snp.SortInstance(4096))
 else:
     arrays = snp.synth_v1(a.q, with_delays=a.workload == "k4")
