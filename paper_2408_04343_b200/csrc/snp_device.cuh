@@ -1276,16 +1276,25 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
     // anything it wrote; the next step's grid may be scheduled right away
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int halted = vc->halted;
-    const long long k = vc->step;
-    if (halted || k >= vc->stop_at) {
+    // one parallel snapshot of the run-control block: every field the
+    // prologue needs arrives in one round trip instead of a chain of
+    // volatile loads per thread (K2's ncu: ~19 % of stall samples sat on
+    // the prologue's Ctrl reads)
+    __shared__ __align__(16) uint32_t ctl_w[(sizeof(Ctrl) + 3) / 4];
+    for (int i = threadIdx.x; i < (int)((sizeof(Ctrl) + 3) / 4); i += blockDim.x)
+        ctl_w[i] = reinterpret_cast<const volatile uint32_t*>(ctl)[i];
+    __syncthreads();
+    const Ctrl* cs = reinterpret_cast<const Ctrl*>(ctl_w);
+    const int halted = cs->halted;
+    const long long k = cs->step;
+    if (halted || k >= cs->stop_at) {
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->push_armed = 0;
         return;
     }
     if (s.p2p && k > 0) {
         // peer exchange: every rank's step k-1 must be in this rank's slot
         __shared__ int x_ok;
-        if (threadIdx.x == 0) x_ok = wait_peers(s, vc->epoch, k - 1) ? 1 : 0;
+        if (threadIdx.x == 0) x_ok = wait_peers(s, cs->epoch, k - 1) ? 1 : 0;
         __syncthreads();
         if (!x_ok) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1308,7 +1317,7 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
         }
         // step k-1 had no selection (k-1 == max_steps): STEP_LIMIT unless a
         // rank saw a negative count when finishing step k-2
-        const bool last = k - 1 >= vc->max_steps;
+        const bool last = k - 1 >= cs->max_steps;
         if (n || last || (!f && !c)) {
             // the LAST CTA to get here publishes the halt: a CTA of this grid
             // that starts late reads Ctrl.halted / Ctrl.step at its top, so an
@@ -1328,12 +1337,12 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
             return;
         }
     }
-    const bool sel = k < vc->max_steps;
-    const int policy = vc->policy;
-    const unsigned long long seed = vc->seed;
-    const int record = LEAN ? 0 : vc->record;
-    const bool stats_on = LEAN ? false : vc->stats_on != 0;
-    const long long slot = k - vc->trace_base;
+    const bool sel = k < cs->max_steps;
+    const int policy = cs->policy;
+    const unsigned long long seed = cs->seed;
+    const int record = LEAN ? 0 : cs->record;
+    const bool stats_on = LEAN ? false : cs->stats_on != 0;
+    const long long slot = k - cs->trace_base;
     const uint32_t* __restrict__ Pprev = pick3(st.P, (k + 2) % 3);
     uint32_t* Pcur = pick3(st.P, k % 3);
     uint32_t* Pzero = pick3(st.P, (k + 1) % 3);
@@ -2196,15 +2205,20 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
     uint32_t* cnt = acc + bin_acc_words<CB>(T);
     E* stage = reinterpret_cast<E*>(cnt + ((NT + 3) & ~3));
     Ctrl* ctl = st.ctrl;
-    const volatile Ctrl* vc = ctl;
-    const int halted = vc->halted;
-    const long long k = vc->step;
-    if (halted || k >= vc->stop_at) return;
-    const bool sel = k < vc->max_steps;
-    const int record = vc->record;
-    const bool stats_on = vc->stats_on != 0;
+    // one parallel snapshot of the run-control block (see tiled_step_kernel)
+    __shared__ __align__(16) uint32_t ctl_w[(sizeof(Ctrl) + 3) / 4];
+    for (int i = threadIdx.x; i < (int)((sizeof(Ctrl) + 3) / 4); i += blockDim.x)
+        ctl_w[i] = reinterpret_cast<const volatile uint32_t*>(ctl)[i];
+    __syncthreads();
+    const Ctrl* cs = reinterpret_cast<const Ctrl*>(ctl_w);
+    const int halted = cs->halted;
+    const long long k = cs->step;
+    if (halted || k >= cs->stop_at) return;
+    const bool sel = k < cs->max_steps;
+    const int record = cs->record;
+    const bool stats_on = cs->stats_on != 0;
     const long long q = s.q;
-    const StepCtx cx{k, k - vc->trace_base, q, vc->seed, nullptr, vc->policy, record, sel, stats_on};
+    const StepCtx cx{k, k - cs->trace_base, q, cs->seed, nullptr, cs->policy, record, sel, stats_on};
     const E* __restrict__ bin_in = reinterpret_cast<const E*>((k & 1) ? st.bins[0] : st.bins[1]);
     E* bin_out = reinterpret_cast<E*>((k & 1) ? st.bins[1] : st.bins[0]);
     uint32_t* fill_in = (k & 1) ? st.bin_fill[0] : st.bin_fill[1];
