@@ -2167,6 +2167,10 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const
 #endif
 constexpr int kBinThreads = SNP_BIN_THREADS;
 constexpr int kBinUnroll = 4;    // column chunks in flight per lane
+#ifndef SNP_BIN_GUNROLL
+#define SNP_BIN_GUNROLL 6
+#endif
+constexpr int kBinGUnroll = SNP_BIN_GUNROLL;  // ELL column-group passes in flight per warp
 
 template <bool UNIT>
 struct BinEntry {
@@ -2358,17 +2362,17 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
                 const uint32_t nf = __popc(fm);
                 if (nch > 0) col_r[warp][__popc(fm & ((1u << lane) - 1u))] = (uint32_t)r;
                 __syncwarp();
-                for (uint32_t i0 = 0; i0 < nf; i0 += per * kBinUnroll) {
-                    int4 v[kBinUnroll];
+                for (uint32_t i0 = 0; i0 < nf; i0 += per * kBinGUnroll) {
+                    int4 v[kBinGUnroll];
 #pragma unroll
-                    for (int u = 0; u < kBinUnroll; ++u) {
+                    for (int u = 0; u < kBinGUnroll; ++u) {
                         const uint32_t col = i0 + u * per + sub;
                         v[u] = make_int4(-1, 0, -1, 0);
                         if (sub < per && col < nf)
                             v[u] = ld_stream16(s.ell + (long long)col_r[warp][col] * s.ell_ld + 2 * cc, pol);
                     }
 #pragma unroll
-                    for (int u = 0; u < kBinUnroll; ++u) {
+                    for (int u = 0; u < kBinGUnroll; ++u) {
                         if (cc > 0 && v[u].x >= 0) deliver((uint32_t)v[u].x, (uint32_t)v[u].y);  // row 0 = consumption
                         if (v[u].z >= 0) deliver((uint32_t)v[u].z, (uint32_t)v[u].w);
                         edges += (cc > 0 && v[u].x >= 0 ? 1u : 0u) + (v[u].z >= 0 ? 1u : 0u);
