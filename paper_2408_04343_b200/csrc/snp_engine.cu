@@ -4,6 +4,7 @@
 // NeuronRuleMap, and either a CSR out-adjacency or the format's own matrix);
 // drives the per-step kernels of snp_device.cuh as CUDA-graph segments with
 // device-side halting; and implements the phase-level entry points.
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu --nvtx (no cost without a tool)
 #include <algorithm>
 #include <chrono>
 #include <cstdarg>
@@ -809,7 +810,10 @@ void launch_main(snp_engine* e) {
 struct PhaseTimer {
     bool on = getenv("SNPB200_TIMING") != nullptr;
     std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    PhaseTimer() { nvtxRangePushA("snp_engine_create"); }
+    ~PhaseTimer() { nvtxRangePop(); }
     void mark(const char* what) {
+        nvtxMarkA(what);
         if (!on) return;
         cudaDeviceSynchronize();
         const auto now = std::chrono::steady_clock::now();
@@ -1863,6 +1867,10 @@ int snp_advance(snp_engine* e, const snp_run_opts* o, int64_t n_steps, snp_trace
         const long long k0 = c.step;
         c.stop_at = k0 + seg;
         c.trace_base = k0;
+        nvtxRangePushA("snp_segment");
+        struct Pop {
+            ~Pop() { nvtxRangePop(); }
+        } pop_on_exit;
         TRY(push_ctrl(e));
         if (e->small_fn) {
             launch_main(e);
