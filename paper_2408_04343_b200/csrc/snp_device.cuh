@@ -2194,31 +2194,6 @@ __host__ __device__ constexpr long long bin_flush_dests(bool unit) {
 template <int CB>
 __host__ __device__ constexpr int bin_acc_words(int T) { return (acc_words<CB>(T) + 3) & ~3; }
 
-// Selection inputs of one light neuron (<= 4 rule words preloaded; more are
-// read by light_commit itself).
-template <bool WIDE>
-struct SelIn {
-    uint32_t r0, nr;
-    long long C;
-    int ds;
-    typename RuleRaw<WIDE>::T w0, w1, w2, w3;
-};
-template <bool WIDE>
-__device__ __forceinline__ SelIn<WIDE> sel_fetch(const DevSys& s, const DevState& st, long long j, bool valid) {
-    SelIn<WIDE> x{};
-    if (valid) {
-        x.r0 = __ldg(s.roff + j);
-        x.nr = __ldg(s.roff + j + 1) - x.r0;
-        x.C = st.cfg[j];
-        x.ds = st.ds[j];
-        if (x.nr > 0) x.w0 = load_raw<WIDE>(s.rw, x.r0);
-        if (x.nr > 1) x.w1 = load_raw<WIDE>(s.rw, x.r0 + 1);
-        if (x.nr > 2) x.w2 = load_raw<WIDE>(s.rw, x.r0 + 2);
-        if (x.nr > 3) x.w3 = load_raw<WIDE>(s.rw, x.r0 + 3);
-    }
-    return x;
-}
-
 // GROUP: ELL column-group walk only (uniform column stride <= 16 chunks);
 // else lane-own / concatenated walks -- separate instances keep the register
 // budget of each (1024 threads: 64 registers) for its own path
@@ -2271,9 +2246,6 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
     unsigned long long edges = 0;
 
     for (int i = threadIdx.x; i < NT; i += kBinThreads) cnt[i] = 0;
-    SelIn<WIDE> pre{};
-    if (blockIdx.x < NT) pre = sel_fetch<WIDE>(s, st, (long long)blockIdx.x * T + threadIdx.x,
-                                               min((long long)T, q - (long long)blockIdx.x * T) > (long long)threadIdx.x);
     for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x) {
         const long long d0 = tile * T;
         const int nd = (int)min((long long)T, q - d0);
@@ -2310,38 +2282,35 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
             fill_in[tile] = 0;
             fill_in[NT + tile] = 0;
         }
-        // ---- B + C (+ D every kWin chunks), kBinThreads destinations at a time.
-        // The selection inputs of a chunk (offsets, Ĉ, delay state, <= 4 rule
-        // words) were loaded one chunk ahead (software pipeline: the loads of
-        // chunk c+1 -- or of the next tile's first chunk -- are in flight
-        // while chunk c walks its columns; nothing the kernel writes before
-        // then touches them)
+        // ---- B + C (+ D every kWin chunks), kBinThreads destinations at a time
         for (int c0 = 0, win = 0; c0 < nd; c0 += kBinThreads, ++win) {
             const int li = c0 + threadIdx.x;
             const long long j = d0 + li;
             int r = -1;
             long long pval = 0;
-            const SelIn<WIDE> cur = pre;
-            {
-                const long long tn = c0 + kBinThreads < nd ? tile : tile + gridDim.x;
-                const int cn = c0 + kBinThreads < nd ? c0 + kBinThreads : 0;
-                if (tn < NT) pre = sel_fetch<WIDE>(s, st, tn * T + cn + threadIdx.x, min((long long)T, q - tn * T) > cn + (long long)threadIdx.x);
-            }
             if (li < nd) {
-                const uint32_t r0 = cur.r0, nr = cur.nr;
-                const long long Cprev = cur.C;
-                const int dsv = cur.ds;
+                const uint32_t r0 = __ldg(s.roff + j), nr = __ldg(s.roff + j + 1) - r0;
+                const long long Cprev = st.cfg[j];
+                const int dsv = st.ds[j];
                 const bool open_prev = ds_open(dsv);
                 const int D = ds_next(dsv);
                 const bool can_sel = sel && D == 0;
+                using Raw = typename RuleRaw<WIDE>::T;
+                Raw w0{}, w1{}, w2{}, w3{};
+                if (can_sel) {
+                    if (nr > 0) w0 = load_raw<WIDE>(s.rw, r0);
+                    if (nr > 1) w1 = load_raw<WIDE>(s.rw, r0 + 1);
+                    if (nr > 2) w2 = load_raw<WIDE>(s.rw, r0 + 2);
+                    if (nr > 3) w3 = load_raw<WIDE>(s.rw, r0 + 3);
+                }
                 long long C = Cprev;
                 if (open_prev) {
                     const uint32_t g = tile_acc_get<CB>(acc, li);
                     C += UNIT ? (long long)g * s.bin_amount : (long long)g;
                 }
-                pval = light_commit<RECV_PULL, P_BIT, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, cur.w0, cur.w1, cur.w2,
-                                                                        cur.w3, C, D, can_sel, stat, t_fired, t_closed,
-                                                                        t_neg, neg_idx, neg_val, r);
+                pval = light_commit<RECV_PULL, P_BIT, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D,
+                                                                        can_sel, stat, t_fired, t_closed, t_neg,
+                                                                        neg_idx, neg_val, r);
             }
             // this lane's column: chunks (ELL: 16-byte pairs of rows, row 0 =
             // consumption, already applied; Optimized: one target per lane)
