@@ -826,12 +826,17 @@ struct PhaseTimer {
 // Dynamic shared memory cap of a kernel: the device's opt-in maximum, not
 // this engine's size -- the attribute is per function, so engines of
 // different sizes in one process must not lower it under each other.
-int allow_max_smem(const void* fn, int device) {
+int allow_max_smem(const void* fn, int device, size_t needed) {
     int optin = 0;
     CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     cudaFuncAttributes fa;
     CU(cudaFuncGetAttributes(&fa, fn));
-    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    const int cap = std::max((int)needed, optin - (int)fa.sharedSizeBytes);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, cap) != cudaSuccess) {
+        cudaGetLastError();  // a tool (e.g. racecheck) may reserve shared memory: fall back to this engine's size
+        if (fa.maxDynamicSharedSizeBytes < (int)needed)
+            CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)needed));
+    }
     return SNP_OK;
 }
 
@@ -1421,7 +1426,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                                      : (unit ? SNP_BIN_PICK(false, false, true, false) : SNP_BIN_PICK(false, false, false, false));
 #undef SNP_BIN_PICK_G
 #undef SNP_BIN_PICK
-                TRY(allow_max_smem((const void*)e->fused_fn, e->device));
+                TRY(allow_max_smem((const void*)e->fused_fn, e->device, smem));
             }
         }
         if (!binned) {
@@ -1516,7 +1521,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             e->small_fn = e->wide_rules ? (r64 ? small_run_kernel<true, true> : small_run_kernel<true, false>)
                                         : (r64 ? small_run_kernel<false, true> : small_run_kernel<false, false>);
             e->small_smem = (size_t)std::max<long long>(1, q) * (r64 ? 8 : 4);
-            TRY(allow_max_smem((const void*)e->small_fn, e->device));
+            TRY(allow_max_smem((const void*)e->small_fn, e->device, e->small_smem));
         }
     } else if (e->format == SNP_FMT_ELL) {
         pick_fns<RECV_ARRAY, P_BIT, false, false>(e->wide_rules, &e->step_fn, &e->prime_fn);
@@ -1532,8 +1537,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                        (size_t)(e->cbits == 8 ? acc_words<8>(s.tile)
                                                  : (e->cbits == 16 ? acc_words<16>(s.tile) : acc_words<32>(s.tile))) *
                            sizeof(uint32_t);
-        TRY(allow_max_smem((const void*)e->step_fn, e->device));
-        TRY(allow_max_smem((const void*)e->lean_fn, e->device));
+        TRY(allow_max_smem((const void*)e->step_fn, e->device, e->step_smem));
+        TRY(allow_max_smem((const void*)e->lean_fn, e->device, e->step_smem));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->step_fn, e->step_block, e->step_smem));
         const long long resident = (long long)std::max(1, per_sm) * std::max(1, n_sm);
         e->step_grid = (int)std::min<long long>(s.n_tiles, resident);
