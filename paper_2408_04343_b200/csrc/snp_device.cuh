@@ -129,6 +129,7 @@ struct DevSys {
     // hx_lut[hx_loff[h] + min(C, len - 1)] = local rule index or ~0
     const uint32_t* hx_loff;
     const uint32_t* hx_lut;
+    const uint16_t* hx_lcnt;  // same indexing: number of applicable rules (saturated at 65535)
     int light_ctas;           // CTAs striding over light tiles
     int heavy_ctas;           // CTAs striding over the heavy list
     long long light_tiles;    // ceil(q / 256)
@@ -690,6 +691,22 @@ __device__ __forceinline__ int heavy_first_applicable_warp(const DevSys& s, int 
         if (i > a0) best = min(best, __ldg(&s.hx_a[i - 1].y));
     }
     return best == 0xffffffffu ? -1 : (int)best;
+}
+
+// SeededRandom through the dense table: when at most one rule is applicable
+// for count C the choice is forced (mix64 % 1 = 0, choose_index), so no scan
+// is needed.  Returns the local rule index, -1 (none applicable) or -2 (no
+// table, or several applicable: scan).
+__device__ __forceinline__ int heavy_seeded_table(const DevSys& s, int h, long long C) {
+    if (C < 0) return -1;
+    if (!s.hx_loff) return -2;
+    const uint32_t l0 = __ldg(s.hx_loff + h), l1 = __ldg(s.hx_loff + h + 1);
+    if (l1 == l0) return -2;
+    const uint32_t c = C >= (long long)(l1 - l0 - 1) ? l1 - l0 - 1 : (uint32_t)C;
+    const uint32_t n = __ldg(s.hx_lcnt + l0 + c);
+    if (n == 0) return -1;
+    if (n > 1) return -2;
+    return (int)__ldg(s.hx_lut + l0 + c);
 }
 
 // SeededRandom over a heavy-rule neuron, one warp: count the applicable
@@ -1739,7 +1756,9 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
                         r = x < 0 ? -1 : (int)(r0 + x);
                         if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                     } else {
-                        r = heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane);
+                        const int x = heavy_seeded_table(s, (int)hh, C);
+                        r = x == -2 ? heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane)
+                                    : (x < 0 ? -1 : (int)(r0 + x));
                         if (lane == 0) stat[ST_SCANNED] += r1 - r0;
                     }
                     if (lane == 0) {
@@ -2602,7 +2621,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
                     r = x < 0 ? -1 : (int)(r0 + x);
                     if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                 } else {
-                    r = heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane);
+                    const int x = heavy_seeded_table(s, h, C);
+                    r = x == -2 ? heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane)
+                                : (x < 0 ? -1 : (int)(r0 + x));
                     if (lane == 0) stat[ST_SCANNED] += r1 - r0;
                 }
                 if (lane == 0) {

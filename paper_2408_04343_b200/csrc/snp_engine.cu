@@ -1205,6 +1205,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         // rule for count c, the last entry for every count above the largest
         // threshold -- one dependent load instead of two 32-ary searches
         std::vector<uint32_t> loff(heavy.size() + 1, 0), lut;
+        std::vector<uint16_t> lcnt;  // applicable rules per count (saturated): SeededRandom's table
         for (size_t h = 0; h < heavy.size(); ++h) {
             const uint32_t i = heavy[h], a = roff[i], b = roff[i + 1];
             uint32_t mt = 0;
@@ -1214,26 +1215,34 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
                 loff[h + 1] = (uint32_t)lut.size();  // no table: the guard index
                 continue;
             }
-            std::vector<uint32_t> exf(mt + 2, 0xffffffffu), alf(mt + 2, 0xffffffffu);
+            std::vector<uint32_t> exf(mt + 2, 0xffffffffu), alf(mt + 2, 0xffffffffu), exn(mt + 2, 0), aln(mt + 2, 0);
             for (uint32_t r = a; r < b; ++r) {
                 const uint32_t t = rthr[r] & ~kExactBit;
-                uint32_t& slot = (rthr[r] & kExactBit) ? exf[t] : alf[t];
+                const bool ex = (rthr[r] & kExactBit) != 0;
+                uint32_t& slot = ex ? exf[t] : alf[t];
                 slot = std::min(slot, r - a);
+                (ex ? exn[t] : aln[t]) += 1;
             }
-            uint32_t best_al = 0xffffffffu;
+            uint32_t best_al = 0xffffffffu, n_al = 0;
             for (uint32_t c = 0; c <= mt; ++c) {
                 best_al = std::min(best_al, alf[c]);
+                n_al += aln[c];
                 lut.push_back(std::min(best_al, exf[c]));
+                lcnt.push_back(std::min<uint32_t>(n_al + exn[c], 0xffffu));
             }
             lut.push_back(best_al);  // counts above every threshold: at-least rules only
+            lcnt.push_back(std::min<uint32_t>(n_al, 0xffffu));
             loff[h + 1] = (uint32_t)lut.size();
         }
         if (!lut.empty()) {
             uint32_t *d_loff, *d_lut;
+            uint16_t* d_lcnt;
             TRY(upload(e, &d_loff, loff));
             TRY(upload(e, &d_lut, lut));
+            TRY(upload(e, &d_lcnt, lcnt));
             s.hx_loff = d_loff;
             s.hx_lut = d_lut;
+            s.hx_lcnt = d_lcnt;
         }
         uint32_t *d_eoff, *d_aoff;
         uint2 *d_ev, *d_av;
