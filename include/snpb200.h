@@ -184,14 +184,17 @@ int snp_engine_create(const snp_system_desc *desc, snp_engine **out);
 void snp_engine_destroy(snp_engine *eng);
 int snp_engine_get_info(const snp_engine *eng, snp_engine_info *info);
 
-/* Reset the run state to `initial` (host [q]; NULL = the system's own
- * initial configuration) with every neuron open (engine.py:427-428). */
+/* Reset the run state to `initial` (int64 [q] in host memory or, through
+ * unified addressing, in device memory -- e.g. a torch CUDA tensor; NULL =
+ * the system's own initial configuration) with every neuron open
+ * (engine.py:427-428). */
 int snp_begin(snp_engine *eng, const int64_t *initial);
 /* Execute up to `n_steps` more steps of the loop of engine.py:441-458,
  * stopping early on halt / error or when `trace` (may be NULL) is full. */
 int snp_advance(snp_engine *eng, const snp_run_opts *opts, int64_t n_steps,
                 snp_trace_out *trace, snp_result *res);
-/* Final state after a halt: C and D (host int64 [q] each; either may be NULL). */
+/* Final state after a halt: C and D (int64 [q] each, host or device memory;
+ * either may be NULL). */
 int snp_read_state(snp_engine *eng, int64_t *config, int64_t *delays);
 /* snp_begin + snp_advance(to halt) + snp_read_state. */
 int snp_run(snp_engine *eng, const int64_t *initial, const snp_run_opts *opts,

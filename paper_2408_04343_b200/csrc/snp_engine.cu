@@ -1836,7 +1836,9 @@ int snp_begin(snp_engine* e, const int64_t* initial) {
     e->hctrl.epoch = ++e->epoch;
     const long long q = e->q;
     const long long* src = initial ? reinterpret_cast<const long long*>(initial) : e->initial.data();
-    if (q > 0) CU(cudaMemcpyAsync(e->st.cfg, src, q * 8, cudaMemcpyHostToDevice, e->stream));
+    // cudaMemcpyDefault (unified addressing): `initial` may be host memory
+    // or a device pointer (e.g. a torch CUDA tensor), copied on the engine's stream
+    if (q > 0) CU(cudaMemcpyAsync(e->st.cfg, src, q * 8, cudaMemcpyDefault, e->stream));
     TRY(push_ctrl(e));
     CU(cudaStreamSynchronize(e->stream));
     e->begun = true;
@@ -1971,14 +1973,15 @@ int snp_read_state(snp_engine* e, int64_t* config, int64_t* delays) {
     CU(cudaSetDevice(e->device));
     const long long q = e->q;
     if (q == 0) return SNP_OK;
-    if (config) CU(cudaMemcpy(config, e->st.cfg, q * 8, cudaMemcpyDeviceToHost));
+    // host or device destinations (cudaMemcpyDefault), ordered on the engine's stream
+    if (config) CU(cudaMemcpyAsync(config, e->st.cfg, q * 8, cudaMemcpyDefault, e->stream));
     if (delays) {
         if (!e->scratch[0]) TRY(e->alloc(&e->scratch[0], q));
         ds_to_delay_kernel<<<grid_for(q), 256, 0, e->stream>>>(q, e->st.ds, e->scratch[0]);
         CU(cudaGetLastError());
-        CU(cudaMemcpyAsync(delays, e->scratch[0], q * 8, cudaMemcpyDeviceToHost, e->stream));
-        CU(cudaStreamSynchronize(e->stream));
+        CU(cudaMemcpyAsync(delays, e->scratch[0], q * 8, cudaMemcpyDefault, e->stream));
     }
+    CU(cudaStreamSynchronize(e->stream));
     return SNP_OK;
 }
 

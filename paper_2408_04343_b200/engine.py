@@ -345,6 +345,24 @@ class DeviceEngine:
         return RunResult(cfg, dly, int(res.steps), reason, res.stats_dict(), int(res.kernel_launches),
                          float(self._lib.snp_last_device_ms(self._h)))
 
+    def run_device(self, max_steps: int, initial, final_config, selection: Selection = FirstApplicable(),
+                   final_delays=None) -> nat.Result:
+        """snp_run with device-resident buffers: ``initial`` / ``final_config`` /
+        ``final_delays`` are int64 CUDA tensors of q elements (anything with
+        ``data_ptr()``); the copies are device-to-device on the engine's
+        stream (no PCIe)."""
+        for t in (initial, final_config) + (() if final_delays is None else (final_delays,)):
+            if t.numel() != self.q or str(t.dtype) != "torch.int64" or not t.is_cuda or not t.is_contiguous():
+                raise ValueError("run_device needs contiguous int64 CUDA tensors of q elements")
+        opts = self._opts(max_steps, selection)
+        res = nat.Result()
+        vp = nat.ctypes.c_void_p
+        rc = self._lib.snp_run(self._h, vp(initial.data_ptr()), nat.ctypes.byref(opts), vp(final_config.data_ptr()),
+                               None if final_delays is None else vp(final_delays.data_ptr()), nat.ctypes.byref(res))
+        if rc:
+            self._raise(rc, res)
+        return res
+
     def time_steps(self, steps: int, selection: Selection = FirstApplicable(), per_kernel: bool = False,
                    collect_stats: bool = False) -> tuple[float, float, nat.Result]:
         """Device-timed segment of ``steps`` steps from the current state."""

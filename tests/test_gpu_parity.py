@@ -589,3 +589,23 @@ def test_binned_push_bucket_overflow(fmt, var):
     res = snp.run_final(prep, snp.SimOptions(max_steps=12, selection=snp.SeededRandom(4)))
     np.testing.assert_array_equal(res.config, want_c)
     np.testing.assert_array_equal(res.delays, want_d)
+
+
+def test_run_with_device_buffers():
+    """snp_begin / snp_read_state take device pointers too (unified
+    addressing): a torch caller runs from and into CUDA tensors with
+    device-to-device copies, bit-identical to the host-buffer run."""
+    import torch
+    a = snp.synth_v1(30_000, with_delays=True)
+    prep = snp.prepare(a, snp.Format.COMPRESSED)
+    init = np.asarray(a.initial, dtype=np.int64) + 3
+    want = snp.run_final(prep, snp.SimOptions(max_steps=9, selection=snp.SeededRandom(2)))  # system's C_0
+    want2 = prep.engine.run_final(9, snp.SeededRandom(2), initial=init)
+    d_init = torch.from_numpy(init).cuda()
+    d_cfg = torch.empty(a.neuron_count, dtype=torch.int64, device="cuda")
+    d_dly = torch.empty_like(d_cfg)
+    res = prep.engine.run_device(9, d_init, d_cfg, snp.SeededRandom(2), final_delays=d_dly)
+    assert int(res.steps) == want2.steps
+    np.testing.assert_array_equal(d_cfg.cpu().numpy(), want2.config)
+    np.testing.assert_array_equal(d_dly.cpu().numpy(), want2.delays)
+    assert not np.array_equal(want.config, want2.config)  # the initial configuration mattered
