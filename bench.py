@@ -241,13 +241,27 @@ def run_ours(args, rank: int, world: int):
     nat.check(lib.snp_run(eng._h, ctypes.c_void_p(host_in.data_ptr()), ctypes.byref(opts_k),
                           ctypes.c_void_p(host_out.data_ptr()), None, ctypes.byref(r)))
     e2e_run_s = time.perf_counter() - t0
+    # the same one-step calls with device buffers (torch CUDA tensors through
+    # unified addressing: device-to-device copies instead of PCIe)
+    dev_in = torch.from_numpy(arrays.initial.copy()).cuda()
+    dev_out = torch.empty(q, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        nat.check(lib.snp_run(eng._h, ctypes.c_void_p(dev_in.data_ptr()), ctypes.byref(opts),
+                              ctypes.c_void_p(dev_out.data_ptr()), None, ctypes.byref(r)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        nat.check(lib.snp_run(eng._h, ctypes.c_void_p(dev_in.data_ptr()), ctypes.byref(opts),
+                              ctypes.c_void_p(dev_out.data_ptr()), None, ctypes.byref(r)))
+        dev_in, dev_out = dev_out, dev_in
+    e2e_dev_s = time.perf_counter() - t0
 
     return {
         "q": q, "m": m, "desc": desc, "gen_s": gen_s, "prep_s": prep_s, "total_ms": total_ms,
         "kernel_ms": kernel_ms, "stats": stats, "stats_steps": nk, "alg_bytes": alg,
         "clocks": clk.summary(), "launches": launches, "info": eng.info,
         "e2e_steps_per_s": e2e_steps / e2e_s, "e2e_bytes": 8 * q, "arrays": arrays,
-        "e2e_run_steps_per_s": args.steps / e2e_run_s,
+        "e2e_run_steps_per_s": args.steps / e2e_run_s, "e2e_device_steps_per_s": e2e_steps / e2e_dev_s,
     }
 
 
@@ -513,7 +527,9 @@ def main():
         "e2e": {"value": r["e2e_steps_per_s"], "unit": unit, "h2d_bytes_per_step": r["e2e_bytes"],
                 "d2h_bytes_per_step": r["e2e_bytes"], "path": "snp_run C ABI, pinned host buffers, 1 step/call",
                 "run_value": r["e2e_run_steps_per_s"],
-                "run_path": f"one snp_run call of {args.steps} steps, host config in / final config out"},
+                "run_path": f"one snp_run call of {args.steps} steps, host config in / final config out",
+                "device_value": r["e2e_device_steps_per_s"],
+                "device_path": "the same 1-step snp_run calls with CUDA-tensor buffers (device-to-device copies)"},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "counters_per_step": {k: v / r["stats_steps"] for k, v in r["stats"].items() if k != "steps"},
