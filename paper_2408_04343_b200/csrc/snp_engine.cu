@@ -195,8 +195,32 @@ struct snp_engine {
 
 namespace {
 
+// Host vectors that every element is written into before being read: the
+// default-initialising allocator skips std::vector's serial zero fill (GBs at
+// 10^8 neurons: the rule records alone are 6.4 GB).
 template <typename T>
-int upload(snp_engine* e, T** dptr, const std::vector<T>& host) {
+struct DefaultInit : std::allocator<T> {
+    template <typename U>
+    struct rebind {
+        using other = DefaultInit<U>;
+    };
+    DefaultInit() = default;
+    template <typename U>
+    DefaultInit(const DefaultInit<U>&) {}
+    template <typename U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <typename U, typename... Args>
+    void construct(U* p, Args&&... args) {
+        ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+};
+template <typename T>
+using hvec = std::vector<T, DefaultInit<T>>;
+
+template <typename T, typename A>
+int upload(snp_engine* e, T** dptr, const std::vector<T, A>& host) {
     TRY(e->alloc(dptr, (long long)host.size()));
     if (!host.empty()) CU(cudaMemcpy(*dptr, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice));
     return SNP_OK;
@@ -223,7 +247,7 @@ struct ShardInput {
     int x_pbits = 0;          // agreed P element width (0: decide from this rank's rules)
     long long x_pmax = 0;     // agreed largest produced amount over every rank
     mutable long long hdr = 128;  // header elements, set once the P width is known
-    std::vector<uint32_t> soff, sdst;  // global out-adjacency
+    hvec<uint32_t> soff, sdst;  // global out-adjacency
     uint32_t xpos(uint32_t src) const {
         return (uint32_t)((src / nl) * (nl + hdr) + src % nl);
     }
@@ -234,8 +258,8 @@ struct ShardInput {
 // CSR out-adjacency is source-major, so a stable bucket pass keeps that
 // order), are packed into 256-edge segments whose sources span < 2^17.
 int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, long long S, bool stage_p);
-int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, const std::vector<uint32_t>& soff,
-                 const std::vector<uint32_t>& sdst, const ShardInput* sh, const std::vector<uint32_t>& roff_h);
+int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, const hvec<uint32_t>& soff,
+                 const hvec<uint32_t>& sdst, const ShardInput* sh, const std::vector<uint32_t>& roff_h);
 
 // Phase-2 stage descriptors of tile t (kSub destinations each, with their
 // rule words when they fit a stage).
@@ -261,12 +285,12 @@ void append_phase2_desc(const snp_engine* e, long long t, const std::vector<uint
     }
 }
 
-int build_tiles(snp_engine* e, const snp_system_desc* d, const std::vector<uint32_t>& soff_in,
-                const std::vector<uint32_t>& sdst_in, const std::vector<uint32_t>& roff_h,
+int build_tiles(snp_engine* e, const snp_system_desc* d, const hvec<uint32_t>& soff_in,
+                const hvec<uint32_t>& sdst_in, const std::vector<uint32_t>& roff_h,
                 std::vector<uint32_t>& heavy, const ShardInput* sh, const uint32_t* d_soff = nullptr,
                 const uint32_t* d_sdst = nullptr) {
-    const std::vector<uint32_t>& soff = sh ? sh->soff : soff_in;
-    const std::vector<uint32_t>& sdst = sh ? sh->sdst : sdst_in;
+    const hvec<uint32_t>& soff = sh ? sh->soff : soff_in;
+    const hvec<uint32_t>& sdst = sh ? sh->sdst : sdst_in;
     const long long lo = sh ? sh->lo : 0, hi = sh ? sh->hi : e->q;
     const long long n_src = sh ? sh->q_global : e->q;
     const long long q = e->q;
@@ -603,8 +627,8 @@ int build_tiles_device(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_
 // source window) on the device; per 32-edge group a tile-order slot block
 // and a window-order offset block; host-side scans of the small per-chunk
 // counts; phase-1 stage descriptors are runs of groups.
-int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, const std::vector<uint32_t>& soff,
-                 const std::vector<uint32_t>& sdst, const ShardInput* sh, const std::vector<uint32_t>& roff_h) {
+int build_tiles2(snp_engine* e, const uint32_t* d_soff, const uint32_t* d_sdst, const hvec<uint32_t>& soff,
+                 const hvec<uint32_t>& sdst, const ShardInput* sh, const std::vector<uint32_t>& roff_h) {
     DevSys& s = e->sys;
     const long long q = e->q, nt = s.n_tiles, T = s.tile;
     if (T > 65535 - 1) return fail(SNP_ERR_CAPACITY, "two-pass tiles need T < 65535");
@@ -859,7 +883,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     // --- rule vector + offsets (matrices.py:48-73, 115-140)
     if (q > 0 && d->offsets[0] != 0) return fail(SNP_ERR_BAD_ARG, "offsets[0] must be 0");
     // +8 tail: the TMA stages of the tiled kernel copy whole 16-byte units
-    std::vector<uint32_t> roff(q + 1 + 8, 0), owner(m);
+    std::vector<uint32_t> roff(q + 1 + 8, 0);
+    hvec<uint32_t> owner(m);  // every rule's owner is written below
     if (parallel_first_fail(q, [&](long long a0, long long a1) -> long long {
             for (long long i = a0; i < a1; ++i) {
                 const long long a = d->offsets[i], b = d->offsets[i + 1];
@@ -871,8 +896,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         }) >= 0)
         return fail(SNP_ERR_BAD_ARG, "offsets not non-decreasing within [0, m]");
     if ((q > 0 ? d->offsets[q] : 0) != m) return fail(SNP_ERR_BAD_ARG, "offsets[q] != m");
-    std::vector<uint32_t> rthr(m);
-    std::vector<int4> rrec(m);
+    hvec<uint32_t> rthr(m);
+    hvec<int4> rrec(m);
     const long long bad_rule = parallel_first_fail(m, [&](long long a, long long b) -> long long {
         for (long long r = a; r < b; ++r) {
             const long long t = d->threshold[r], c = d->consumed[r], p = d->produced[r], dl = d->delay[r];
@@ -892,16 +917,42 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             return fail(SNP_ERR_CAPACITY, "rule %lld consumed/produced outside [0, 2^31-1]", r);
         return fail(SNP_ERR_CAPACITY, "rule %lld delay %lld outside [0, 2^31-3]", r, dl);
     }
+    // compact rule words possible? largest / common produced amount (one
+    // pass per host thread, then merged in order)
     bool compact = true;
     long long pmax = 0, pfirst = -1;
     bool pcommon = true;
-    for (long long r = 0; r < m; ++r) {
-        const int4 x = rrec[r];
-        if (x.x >= 65536 || x.y >= 256 || x.z >= 256) compact = false;
-        if (x.y > 0) {
-            pmax = std::max<long long>(pmax, x.y);
-            if (pfirst < 0) pfirst = x.y;
-            else if (x.y != pfirst) pcommon = false;
+    {
+        const int nt = (int)std::max<long long>(1, std::min<long long>(std::max(1u, std::thread::hardware_concurrency()),
+                                                                       m / (1 << 16) + 1));
+        struct Part {
+            bool compact = true, pcommon = true;
+            long long pmax = 0, pfirst = -1;
+        };
+        std::vector<Part> parts(nt);
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                Part& P = parts[t];
+                for (long long r = m * t / nt; r < m * (t + 1) / nt; ++r) {
+                    const int4 x = rrec[r];
+                    if (x.x >= 65536 || x.y >= 256 || x.z >= 256) P.compact = false;
+                    if (x.y > 0) {
+                        P.pmax = std::max<long long>(P.pmax, x.y);
+                        if (P.pfirst < 0) P.pfirst = x.y;
+                        else if (x.y != P.pfirst) P.pcommon = false;
+                    }
+                }
+            });
+        for (auto& x : th) x.join();
+        for (const Part& P : parts) {
+            compact = compact && P.compact;
+            pmax = std::max(pmax, P.pmax);
+            pcommon = pcommon && P.pcommon;
+            if (P.pfirst >= 0) {
+                if (pfirst < 0) pfirst = P.pfirst;
+                else if (P.pfirst != pfirst) pcommon = false;
+            }
         }
     }
 
@@ -924,7 +975,7 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
 
     tm.mark("rule vector");
     // --- transition structure
-    std::vector<uint32_t> soff, sdst;
+    hvec<uint32_t> soff, sdst;
     bool have_adj = false;
     if (d->adj_offsets) {
         soff.resize(q + 1);
@@ -932,7 +983,10 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         const long long S = q > 0 ? d->adj_offsets[q] : 0;
         if (S >= (1ll << 32) - 1) return fail(SNP_ERR_CAPACITY, "synapse count %lld exceeds uint32", S);
         sdst.resize(S);
-        for (long long i = 0; i <= q; ++i) soff[i] = (uint32_t)d->adj_offsets[i];
+        parallel_first_fail(q + 1, [&](long long a, long long b) -> long long {
+            for (long long i = a; i < b; ++i) soff[i] = (uint32_t)d->adj_offsets[i];
+            return -1;
+        });
         const long long bad = parallel_first_fail(S, [&](long long a, long long b) -> long long {
             for (long long x = a; x < b; ++x) {
                 const long long t = d->adj_targets[x];
@@ -1077,7 +1131,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
     s.outdeg = d_outdeg;
     e->wide_rules = !compact;
     if (compact) {
-        std::vector<uint2> rw(m + 2);  // +2: 16-byte bulk-copy tails
+        hvec<uint2> rw(m + 2);  // +2: 16-byte bulk-copy tails (written below)
+        rw[m] = rw[m + 1] = make_uint2(0, 0);
         parallel_first_fail(m, [&](long long a, long long b) -> long long {
             for (long long r = a; r < b; ++r)
                 rw[r] = make_uint2(rthr[r], (uint32_t)rrec[r].x | ((uint32_t)rrec[r].y << 16) | ((uint32_t)rrec[r].z << 24));
@@ -1104,7 +1159,8 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         }) < 0;
         if (const char* env = getenv("SNPB200_TINY")) tiny = tiny && atoi(env) != 0;
         if (tiny) {
-            std::vector<uint32_t> rw4(m + 4);  // +4: 16-byte bulk-copy tails
+            hvec<uint32_t> rw4(m + 4);  // +4: 16-byte bulk-copy tails
+            for (int x = 0; x < 4; ++x) rw4[m + x] = 0u;
             parallel_first_fail(m, [&](long long a, long long b) -> long long {
                 for (long long r = a; r < b; ++r)
                     rw4[r] = tiny_word(rthr[r], (uint32_t)rrec[r].x, (uint32_t)rrec[r].y, (uint32_t)rrec[r].z);
@@ -1773,12 +1829,19 @@ int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
             return fail(SNP_ERR_CAPACITY, "row partition exceeds 32-bit exchange positions");
         sh.soff.resize(q + 1);
         sh.sdst.resize(S);
-        for (long long i = 0; i <= q; ++i) sh.soff[i] = (uint32_t)desc->adj_offsets[i];
-        for (long long x = 0; x < S; ++x) {
-            const long long t = desc->adj_targets[x];
-            if (t < 0 || t >= q) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", t);
-            sh.sdst[x] = (uint32_t)t;
-        }
+        parallel_first_fail(q + 1, [&](long long a, long long b) -> long long {
+            for (long long i = a; i < b; ++i) sh.soff[i] = (uint32_t)desc->adj_offsets[i];
+            return -1;
+        });
+        const long long bad = parallel_first_fail(S, [&](long long a, long long b) -> long long {
+            for (long long x = a; x < b; ++x) {
+                const long long t = desc->adj_targets[x];
+                if (t < 0 || t >= q) return x;
+                sh.sdst[x] = (uint32_t)t;
+            }
+            return -1;
+        });
+        if (bad >= 0) return fail(SNP_ERR_BAD_ARG, "synapse target %lld out of range", (long long)desc->adj_targets[bad]);
         // node arrays (initial, offsets, rules) describe this rank's neurons
         // [lo, hi) only; `m` counts their rules
         snp_system_desc ld = *desc;
