@@ -609,3 +609,34 @@ def test_run_with_device_buffers():
     np.testing.assert_array_equal(d_cfg.cpu().numpy(), want2.config)
     np.testing.assert_array_equal(d_dly.cpu().numpy(), want2.delays)
     assert not np.array_equal(want.config, want2.config)  # the initial configuration mattered
+
+
+@pytest.mark.parametrize("fmt,variant", FORMATS + [(snp.Format.COMPRESSED, "tiled2")],
+                         ids=FMT_IDS + ["compressed-tiled2"])
+def test_edge_systems_every_variant(fmt, variant):
+    """Degenerate inputs the reference accepts (engine.py:416-461): no
+    neurons, one neuron without rules, a neuron whose only rule never
+    applies, and a two-neuron loop that only stops at the step limit."""
+    cases = []
+    cases.append((snp.SNPSystem().validate(), 3, snp.HaltReason.NO_APPLICABLE_RULES, [[]]))
+    s = snp.SNPSystem()
+    s.add_neuron(5)
+    cases.append((s.validate(), 10, snp.HaltReason.NO_APPLICABLE_RULES, [[5]]))
+    s = snp.SNPSystem()
+    a = s.add_neuron(2)
+    s.add_rule(a, snp.exactly(3), 1, 1, 0)
+    cases.append((s.validate(), 10, snp.HaltReason.NO_APPLICABLE_RULES, [[2]]))
+    s = snp.SNPSystem()
+    x, y = s.add_neuron(1), s.add_neuron(0)
+    s.add_rule(x, snp.at_least(1), 1, 1, 0)
+    s.add_rule(y, snp.at_least(1), 1, 1, 0)
+    s.add_synapse(x, y)
+    s.add_synapse(y, x)
+    cases.append((s.validate(), 4, snp.HaltReason.STEP_LIMIT, [[1, 0], [0, 1], [1, 0], [0, 1], [1, 0]]))
+    for system, L, halt, configs in cases:
+        tr = snp.simulate_prepared(snp.prepare(system, fmt, variant=variant),
+                                   snp.SimOptions(max_steps=L, record=snp.RecordLevel.FULL))
+        assert tr.halt_reason is halt, (system.neuron_count, tr.halt_reason)
+        assert [c.tolist() for c in tr.configs] == configs
+        ref = snp.simulate(system, snp.Format.COMPRESSED, snp.SimOptions(max_steps=L, record=snp.RecordLevel.FULL))
+        assert trace_digest(tr.configs, tr.delays, tr.spiking) == trace_digest(ref.configs, ref.delays, ref.spiking)
