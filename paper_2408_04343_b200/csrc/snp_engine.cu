@@ -1069,6 +1069,10 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
         // small systems: one CTA runs whole loop segments (small_run_kernel)
         const bool small_ok = !sh && q <= kSmallMaxQ && (long long)sdst.size() + m <= (1ll << 17);
         if (e->variant == SNP_VARIANT_AUTO && small_ok && q > 0) e->variant = SNP_VARIANT_SMALL;
+        // no neurons: nothing to tile (a zero-CTA grid never decides the
+        // halt); the one-CTA kernel decides NO_APPLICABLE_RULES at step 0
+        if (q == 0 && !sh && e->variant != SNP_VARIANT_PULL && e->variant != SNP_VARIANT_PUSH)
+            e->variant = SNP_VARIANT_SMALL;
         if (e->variant == SNP_VARIANT_SMALL && (sh || q > kSmallMaxQ))
             return fail(SNP_ERR_BAD_ARG, "variant SMALL needs an unpartitioned system of <= %lld neurons", kSmallMaxQ);
         if (e->variant == SNP_VARIANT_AUTO) {
