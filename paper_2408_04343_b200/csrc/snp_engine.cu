@@ -1825,6 +1825,9 @@ int snp_engine_create(const snp_system_desc* desc, snp_engine** out) {
         sh.nl = (ceil_div(std::max<long long>(q, 1), desc->world) + 127) / 128 * 128;
         sh.lo = std::min<long long>(q, (long long)desc->rank * sh.nl);
         sh.hi = std::min<long long>(q, sh.lo + sh.nl);
+        if (sh.hi <= sh.lo)
+            return fail(SNP_ERR_BAD_ARG, "row partition: rank %d of %d owns no neurons (q=%lld; rows are cut in "
+                        "multiples of 128): use fewer ranks", (int)desc->rank, (int)desc->world, q);
         TRY(check_csr_offsets(desc->adj_offsets, q));
         const long long S = q > 0 ? desc->adj_offsets[q] : 0;
         sh.x_pbits = desc->x_pbits;

@@ -552,3 +552,15 @@ def test_nccl_allgather_exchange_runs():
         assert cfg == want.config.tolist() and dly == want.delays.tolist(), case
         assert steps == want.steps and reason == str(want.halt_reason), case
         assert launches >= steps
+
+
+@pytest.mark.gpu
+def test_partition_rank_without_rows_is_rejected():
+    """Rows are cut in multiples of 128: q=100 over 2 ranks leaves rank 1
+    empty, which the engine refuses (a zero-tile grid could never take the
+    halting decision) instead of hanging."""
+    a = snp.synth_v1(100)
+    lay = shd.shard_layout(100, 2)
+    assert lay.bounds(1)[0] == lay.bounds(1)[1]
+    with pytest.raises(ValueError, match="owns no neurons"):
+        shd.ShardedEngine(shd.local_arrays(a, lay, 1), 100, 1, 2, p_span=shd.p_range(a.rules))
