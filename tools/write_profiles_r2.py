@@ -19,7 +19,11 @@ CAPS = [("k3_tiled", "k3/compressed/tiled/first", "K3 synth q=1e7, Optimized (ti
         ("k3_ell", "k3/ell/tiled/first", "K3 synth q=1e7, ELL (Alg. 4) binned push step kernel"),
         ("k3_push", "k3/compressed/push/first", "K3 synth q=1e7, COMPRESSED push (Alg. 5) binned step kernel"),
         ("k3_pull", "k3/compressed/pull/first", "K3 synth q=1e7, COMPRESSED CSR-pull step kernel"),
-        ("sort100_small", "sort100/compressed/small/first", "sort n=100, small-system kernel (one launch = 6 steps)")]
+        ("sort100_small", "sort100/compressed/small/first", "sort n=100, small-system kernel (one launch = 6 steps)"),
+        ("k3_tiled2_pass1", "k3tp/compressed/tiled2/pass1", "K3, two-pass receive (variant tiled2): pass 1 per source window"),
+        ("k3_tiled2_tiles", "k3tp/compressed/tiled2/tiles", "K3, two-pass receive (variant tiled2): the tile kernel"),
+        ("sort2048_dense", "sort2048/sparse/dense", "sort n=2048, SPARSE (dense GEMV over fired rows, Alg. 3)"),
+        ("sort2048_dense_step", "sort2048/sparse/step", "sort n=2048, SPARSE: the fused finish/select step kernel")]
 
 
 def dram_bytes(summary: str) -> float:
@@ -44,7 +48,7 @@ def main():
         if "gpu__time_duration" not in summ:
             continue
         b = dram_bytes(summ)
-        if key.startswith(("k2", "k3", "k4", "k5")):
+        if key.startswith(("k2/", "k3/", "k4/", "k5/")):
             traffic[key] = b
         log = (GP / f"{name}.log").read_text() if (GP / f"{name}.log").exists() else ""
         info = [l for l in log.splitlines() if "ms/step" in l]
