@@ -1287,7 +1287,6 @@ __global__ void __launch_bounds__(kTileThreads + 32, 1) tiled_step_kernel(const 
     __shared__ __align__(8) uint64_t empty_bar[kMaxRing];
     __shared__ __align__(16) StageDesc desc_s[32];
     Ctrl* ctl = st.ctrl;
-    const volatile Ctrl* vc = ctl;
     // launched with programmatic stream serialization: wait for the previous
     // step's grid to complete (and its writes to be visible) before reading
     // anything it wrote; the next step's grid may be scheduled right away
