@@ -2531,15 +2531,20 @@ __global__ void __launch_bounds__(kBinThreads, 1) ell_bin_step_kernel(const __gr
 //   D. halting decision for step k (finish_step's rules), then the next step.
 constexpr int kSmallThreads = 1024;
 constexpr long long kSmallMaxQ = 16384;   // 128 KB of int64 receive counters
+constexpr long long kSmallSmemQ = 4096;   // state in shared memory too: 4096 x (8 + 4 + 4 + 8) B
 
 #ifndef SNP_TEMPLATES_ONLY
 // R64: 64-bit receive counters (some destination can receive >= 2^31 in one
 // step); else 32-bit, whose shared-memory atomics are native
-template <bool WIDE, bool R64>
+// SMEM: the state itself (Ĉ, delay state, chosen rule) lives in shared memory
+// for the whole launch (q <= kSmallSmemQ): every step's reads and writes of it
+// are shared-memory accesses instead of L2 round trips
+template <bool WIDE, bool R64, bool SMEM>
 __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __grid_constant__ DevSys s, DevState st) {
     using RT = typename std::conditional<R64, unsigned long long, unsigned int>::type;
     extern __shared__ __align__(128) uint8_t smem[];
     RT* recv_s = reinterpret_cast<RT*>(smem);  // [q] deliveries of the previous step
+    DevState sl = st;                          // the state the steps read and write
     __shared__ long long sh_neg_idx, sh_neg_val;
     __shared__ int sh_go;
     Ctrl* ctl = st.ctrl;
@@ -2556,6 +2561,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
     const bool stats_on = vc->stats_on != 0;
     const unsigned long long seed = vc->seed;
     long long k = vc->step;
+    if (SMEM) {
+        const size_t o = ((size_t)q * sizeof(RT) + 15) & ~(size_t)15;
+        sl.cfg = reinterpret_cast<long long*>(smem + o);
+        sl.ds = reinterpret_cast<int*>(smem + o + (size_t)q * 8);
+        sl.chosen = reinterpret_cast<int*>(smem + o + (size_t)q * 12);
+        for (long long j = threadIdx.x; j < q; j += kSmallThreads) {
+            sl.cfg[j] = st.cfg[j];
+            sl.ds[j] = st.ds[j];
+            sl.chosen[j] = st.chosen[j];
+        }
+    }
     for (long long j = threadIdx.x; j < q; j += kSmallThreads) recv_s[j] = (RT)st.recv[j];
     __syncthreads();
     for (;;) {
@@ -2569,9 +2585,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
         // ---- A
         for (long long j = threadIdx.x; j < q; j += kSmallThreads) {
             const uint32_t r0 = __ldg(s.roff + j), nr = __ldg(s.roff + j + 1) - r0;
-            const int dsv = st.ds[j];
+            const int dsv = sl.ds[j];
             const int D = ds_next(dsv);
-            long long C = st.cfg[j];
+            long long C = sl.cfg[j];
             const long long rv = R64 ? (long long)recv_s[j] : (long long)(int)recv_s[j];
             recv_s[j] = 0;
             if (ds_open(dsv)) C += rv;
@@ -2584,10 +2600,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
                 if (record & REC_CONFIGS) st.tr_cfg[cx.slot * q + j] = C;
                 if (record & REC_DELAYS) st.tr_dly[cx.slot * q + j] = D;
                 t_closed |= D != 0;
-                st.cfg[j] = C;
-                st.ds[j] = D;
+                sl.cfg[j] = C;
+                sl.ds[j] = D;
                 if (sel) {
-                    st.chosen[j] = -1;
+                    sl.chosen[j] = -1;
                     if (record & REC_SPIKING) st.tr_chosen[cx.slot * q + j] = -1;
                 }
             } else {
@@ -2601,7 +2617,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
                 }
                 int r = -1;
                 long long ni = neg_idx, nv = neg_val;
-                light_commit<RECV_ARRAY, P_BIT, true, false, WIDE>(s, st, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D, can_sel,
+                light_commit<RECV_ARRAY, P_BIT, true, false, WIDE>(s, sl, ctl, cx, j, r0, nr, w0, w1, w2, w3, C, D, can_sel,
                                                                    stat, t_fired, t_closed, t_neg, ni, nv, r);
                 if (ni < neg_idx) neg_idx = ni, neg_val = nv;
             }
@@ -2611,8 +2627,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
         if (sel) {
             for (int h = warp; h < s.n_heavy; h += kSmallThreads / 32) {
                 const long long j = s.heavy[h];
-                if (st.ds[j] != 0) continue;  // D_k (A stored it): closed
-                const long long C = st.cfg[j];
+                if (sl.ds[j] != 0) continue;  // D_k (A stored it): closed
+                const long long C = sl.cfg[j];
                 const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
                 int r;
                 if (policy == 0) {
@@ -2629,9 +2645,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
                     stat[ST_OPEN] += 1;
                     if (r >= 0) {
                         const uint4 wr = load_rule<WIDE>(s.rw, r);
-                        st.cfg[j] = C - (long long)wr.y;
-                        st.ds[j] = -((int)wr.w + 1);
-                        st.chosen[j] = r;
+                        sl.cfg[j] = C - (long long)wr.y;
+                        sl.ds[j] = -((int)wr.w + 1);
+                        sl.chosen[j] = r;
                         t_fired = true;
                         stat[ST_FIRED] += 1;
                         if (wr.z > 0) {
@@ -2650,7 +2666,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
         // ---- C (one warp per fired neuron, lanes over its out-edges)
         if (sel) {
             for (long long j = warp; j < q; j += kSmallThreads / 32) {
-                const int r = st.chosen[j];
+                const int r = sl.chosen[j];
                 if (r < 0) continue;
                 const int p = __ldg(&s.rrec[r].y);
                 if (p <= 0) continue;
@@ -2698,8 +2714,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
         if (!sh_go) break;
         ++k;
     }
-    for (long long j = threadIdx.x; j < q; j += kSmallThreads)
+    for (long long j = threadIdx.x; j < q; j += kSmallThreads) {
         st.recv[j] = R64 ? (long long)recv_s[j] : (long long)(int)recv_s[j];
+        if (SMEM) {
+            st.cfg[j] = sl.cfg[j];
+            st.ds[j] = sl.ds[j];
+            st.chosen[j] = sl.chosen[j];
+        }
+    }
     __threadfence();
 }
 #endif  // SNP_TEMPLATES_ONLY

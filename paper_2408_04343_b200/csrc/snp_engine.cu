@@ -1587,9 +1587,13 @@ int build(snp_engine* e, const snp_system_desc* d, const ShardInput* sh = nullpt
             uint32_t mx = 0;
             for (uint32_t t : sdst) mx = std::max(mx, ++ind[t]);
             const bool r64 = (double)mx * (double)std::max<long long>(1, pmax) >= 2147483648.0;
-            e->small_fn = e->wide_rules ? (r64 ? small_run_kernel<true, true> : small_run_kernel<true, false>)
-                                        : (r64 ? small_run_kernel<false, true> : small_run_kernel<false, false>);
-            e->small_smem = (size_t)std::max<long long>(1, q) * (r64 ? 8 : 4);
+            const bool sm = q <= kSmallSmemQ;  // the state in shared memory too
+#define SNP_SMALL_PICK(W_) (r64 ? (sm ? small_run_kernel<W_, true, true> : small_run_kernel<W_, true, false>) \
+                                : (sm ? small_run_kernel<W_, false, true> : small_run_kernel<W_, false, false>))
+            e->small_fn = e->wide_rules ? SNP_SMALL_PICK(true) : SNP_SMALL_PICK(false);
+#undef SNP_SMALL_PICK
+            const size_t rb = (((size_t)std::max<long long>(1, q) * (r64 ? 8 : 4)) + 15) & ~(size_t)15;
+            e->small_smem = rb + (sm ? (size_t)std::max<long long>(1, q) * 16 : 0);
             TRY(allow_max_smem((const void*)e->small_fn, e->device, e->small_smem));
         }
     } else if (e->format == SNP_FMT_ELL) {
