@@ -664,6 +664,18 @@ __device__ __forceinline__ uint32_t warp_bound(const uint2* __restrict__ keys, u
     return lo + __popc(__ballot_sync(0xffffffffu, below));
 }
 
+// FirstApplicable from the dense table alone (one thread): local rule index,
+// -1 (none applicable), or -2 (this neuron has no table).
+__device__ __forceinline__ int heavy_first_table(const DevSys& s, int h, long long C) {
+    if (C < 0) return -1;
+    if (!s.hx_loff) return -2;
+    const uint32_t l0 = __ldg(s.hx_loff + h), l1 = __ldg(s.hx_loff + h + 1);
+    if (l1 == l0) return -2;
+    const uint32_t c = C >= (long long)(l1 - l0 - 1) ? l1 - l0 - 1 : (uint32_t)C;
+    const uint32_t v = __ldg(s.hx_lut + l0 + c);
+    return v == 0xffffffffu ? -1 : (int)v;
+}
+
 // heavy_first_applicable, one warp (all lanes get the answer).
 __device__ __forceinline__ int heavy_first_applicable_warp(const DevSys& s, int h, long long C, int lane) {
     if (C < 0) return -1;
@@ -2623,42 +2635,62 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_run_kernel(const __gri
             }
         }
         __syncthreads();
-        // ---- B
+        // ---- B: heavy neurons.  B1, thread per neuron: the dense tables answer
+        // FirstApplicable, and SeededRandom when the choice is forced; B2,
+        // warp per neuron, scans what the tables leave open (marked -3).
+        auto commit_heavy = [&](long long j, long long C, uint32_t r0, uint32_t r1, int r, bool scanned_all) {
+            stat[ST_SCANNED] += scanned_all ? r1 - r0 : ((r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0);
+            stat[ST_OPEN] += 1;
+            if (r >= 0) {
+                const uint4 wr = load_rule<WIDE>(s.rw, r);
+                sl.cfg[j] = C - (long long)wr.y;
+                sl.ds[j] = -((int)wr.w + 1);
+                sl.chosen[j] = r;
+                t_fired = true;
+                stat[ST_FIRED] += 1;
+                if (wr.z > 0) {
+                    stat[ST_SENDING] += 1;
+                    if (stats_on) {
+                        const uint32_t od = __ldg(s.outdeg + j);
+                        stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
+                    }
+                }
+                if (record & REC_SPIKING) st.tr_chosen[cx.slot * q + j] = r;
+            }
+        };
+        bool any_scan = false;
         if (sel) {
-            for (int h = warp; h < s.n_heavy; h += kSmallThreads / 32) {
+            for (int h = threadIdx.x; h < s.n_heavy; h += kSmallThreads) {
                 const long long j = s.heavy[h];
                 if (sl.ds[j] != 0) continue;  // D_k (A stored it): closed
+                const long long C = sl.cfg[j];
+                const int x = policy == 0 ? heavy_first_table(s, h, C) : heavy_seeded_table(s, h, C);
+                if (x == -2) {
+                    sl.chosen[j] = -3;  // B2 scans it
+                    any_scan = true;
+                    continue;
+                }
+                const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
+                commit_heavy(j, C, r0, r1, x < 0 ? -1 : (int)(r0 + x), policy != 0);
+            }
+        }
+        if (__syncthreads_or(any_scan)) {
+            for (int h = warp; h < s.n_heavy; h += kSmallThreads / 32) {
+                const long long j = s.heavy[h];
+                if (sl.chosen[j] != -3) continue;
                 const long long C = sl.cfg[j];
                 const uint32_t r0 = __ldg(s.roff + j), r1 = __ldg(s.roff + j + 1);
                 int r;
                 if (policy == 0) {
                     const int x = heavy_first_applicable_warp(s, h, C, lane);
                     r = x < 0 ? -1 : (int)(r0 + x);
-                    if (lane == 0) stat[ST_SCANNED] += (r >= 0) ? (uint32_t)r - r0 + 1 : r1 - r0;
                 } else {
-                    const int x = heavy_seeded_table(s, h, C);
-                    r = x == -2 ? heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane)
-                                : (x < 0 ? -1 : (int)(r0 + x));
-                    if (lane == 0) stat[ST_SCANNED] += r1 - r0;
+                    r = heavy_seeded_warp<WIDE>(s, r0, r1, C, seed, k, j + s.gbase, lane);
                 }
+                __syncwarp();
                 if (lane == 0) {
-                    stat[ST_OPEN] += 1;
-                    if (r >= 0) {
-                        const uint4 wr = load_rule<WIDE>(s.rw, r);
-                        sl.cfg[j] = C - (long long)wr.y;
-                        sl.ds[j] = -((int)wr.w + 1);
-                        sl.chosen[j] = r;
-                        t_fired = true;
-                        stat[ST_FIRED] += 1;
-                        if (wr.z > 0) {
-                            stat[ST_SENDING] += 1;
-                            if (stats_on) {
-                                const uint32_t od = __ldg(s.outdeg + j);
-                                stat[ST_ROWS] += od + (od < (uint32_t)s.z ? 1u : 0u);
-                            }
-                        }
-                        if (record & REC_SPIKING) st.tr_chosen[cx.slot * q + j] = r;
-                    }
+                    sl.chosen[j] = -1;
+                    commit_heavy(j, C, r0, r1, r, policy != 0);
                 }
             }
         }
