@@ -235,8 +235,15 @@ int snp_exchange_info(const snp_engine *eng, snp_exchange *x);
 /* Launch on the caller's CUDA stream (cudaStream_t passed as void*; NULL =
  * the engine's own stream), e.g. the stream NCCL runs on. */
 int snp_set_stream(snp_engine *eng, void *stream);
-/* After snp_begin: run parameters for snp_launch_step. */
+/* After snp_begin: run parameters for snp_launch_step.  With record flags
+ * (SNP_REC_CONFIGS / DELAYS / SPIKING) every row of the run is kept on the
+ * device (max_steps + 2 rows) for snp_read_trace. */
 int snp_configure(snp_engine *eng, const snp_run_opts *opts);
+/* Rows [first_row, first_row + n_rows) of a configured recording run
+ * (row k = the state after k steps; this engine's neurons; chosen = this
+ * engine's rule indices or -1).  Host int64 [n_rows][q] each; NULL skips. */
+int snp_read_trace(snp_engine *eng, int64_t first_row, int64_t n_rows, int64_t *configs,
+                   int64_t *delays, int64_t *chosen);
 /* Enqueue one step (no host synchronisation). */
 int snp_launch_step(snp_engine *eng);
 /* Synchronise the engine stream and read the run state. */

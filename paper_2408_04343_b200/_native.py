@@ -121,6 +121,8 @@ SIGNATURES = [
     ("snp_set_stream", ctypes.c_int, [_EngineP, ctypes.c_void_p]),
     ("snp_configure", ctypes.c_int, [_EngineP, ctypes.POINTER(RunOpts)]),
     ("snp_launch_step", ctypes.c_int, [_EngineP]),
+    ("snp_read_trace", ctypes.c_int, [_EngineP, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p]),
     ("snp_poll", ctypes.c_int, [_EngineP, ctypes.POINTER(Result)]),
     ("snp_engine_layout_digest", ctypes.c_int, [_EngineP, ctypes.c_void_p]),
     ("snp_exchange_ipc_handle", ctypes.c_int, [_EngineP, ctypes.c_void_p]),

@@ -2304,12 +2304,40 @@ int snp_configure(snp_engine* e, const snp_run_opts* o) {
     c.max_steps = o->max_steps;
     c.policy = o->policy;
     c.seed = o->seed;
-    c.record = 0;
+    // recording (row partitions, snp_read_trace): every row of the run stays
+    // in the device ring -- step k's rows at slot k (trace_base 0)
+    const int rec = o->record & (SNP_REC_CONFIGS | SNP_REC_DELAYS | SNP_REC_SPIKING);
+    if (rec) TRY(ensure_trace(e, o->max_steps + 2));
+    c.record = rec;
     c.stats_on = o->collect_stats ? 1 : 0;
     c.stop_at = 0x3fffffffffffffffll;
     c.trace_base = 0;
     TRY(push_ctrl(e));
     CU(cudaStreamSynchronize(e->stream));
+    return SNP_OK;
+}
+
+int snp_read_trace(snp_engine* e, int64_t first_row, int64_t n_rows, int64_t* configs, int64_t* delays,
+                   int64_t* chosen) {
+    if (!e) return fail(SNP_ERR_BAD_ARG, "null engine");
+    if (!e->hctrl.record) return fail(SNP_ERR_BAD_ARG, "snp_read_trace needs a run configured with record flags");
+    if (first_row < 0 || n_rows < 0 || first_row + n_rows > e->tr_rows)
+        return fail(SNP_ERR_BAD_ARG, "trace rows [%lld, %lld) outside the ring of %lld", (long long)first_row,
+                    (long long)(first_row + n_rows), e->tr_rows);
+    CU(cudaSetDevice(e->device));
+    CU(cudaStreamSynchronize(e->stream));
+    const long long q = e->q, n = n_rows * q, o = first_row * q;
+    if (n == 0) return SNP_OK;
+    if (configs) CU(cudaMemcpy(configs, e->st.tr_cfg + o, n * 8, cudaMemcpyDefault));
+    std::vector<int> tmp;
+    auto widen = [&](const int* src, int64_t* dst) -> int {
+        tmp.resize((size_t)n);
+        CU(cudaMemcpy(tmp.data(), src + o, n * 4, cudaMemcpyDeviceToHost));
+        for (long long i = 0; i < n; ++i) dst[i] = tmp[i];
+        return SNP_OK;
+    };
+    if (delays) TRY(widen(e->st.tr_dly, delays));
+    if (chosen) TRY(widen(e->st.tr_chosen, chosen));
     return SNP_OK;
 }
 

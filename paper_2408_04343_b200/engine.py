@@ -386,11 +386,29 @@ class DeviceEngine:
     def set_stream(self, stream_ptr: int | None) -> None:
         nat.check(self._lib.snp_set_stream(self._h, nat.ctypes.c_void_p(stream_ptr or 0)))
 
-    def configure(self, max_steps: int, selection: Selection, collect_stats: bool = False) -> None:
-        opts = self._opts(max_steps, selection, collect_stats=collect_stats)
+    def configure(self, max_steps: int, selection: Selection, collect_stats: bool = False, record: int = 0) -> None:
+        """Run parameters for launch_step; ``record`` (SNP_REC_* flags) keeps
+        every row of the run on the device for read_trace."""
+        opts = self._opts(max_steps, selection, record=int(record), collect_stats=collect_stats)
         rc = self._lib.snp_configure(self._h, nat.ctypes.byref(opts))
         if rc:
             self._raise(rc)
+
+    def read_trace(self, n_configs: int, n_spiking: int, record: int):
+        """Rows 0..n_configs-1 (configs / delays) and 0..n_spiking-1 (chosen,
+        this engine's rule indices or -1) of a recording run."""
+        q = self.q
+        cfg = np.empty((n_configs, q), np.int64) if record & nat.SNP_REC_CONFIGS else None
+        dly = np.empty((n_configs, q), np.int64) if record & nat.SNP_REC_DELAYS else None
+        ch = np.empty((n_spiking, q), np.int64) if record & nat.SNP_REC_SPIKING else None
+        rc = self._lib.snp_read_trace(self._h, 0, n_configs, nat.ptr(cfg), nat.ptr(dly), None)
+        if rc:
+            self._raise(rc)
+        if ch is not None and n_spiking:
+            rc = self._lib.snp_read_trace(self._h, 0, n_spiking, None, None, nat.ptr(ch))
+            if rc:
+                self._raise(rc)
+        return cfg, dly, ch
 
     def layout_digest(self) -> tuple[int, ...]:
         """Digests of the tiled layout arrays (snp_engine_layout_digest)."""

@@ -29,7 +29,7 @@ from typing import Callable
 
 import numpy as np
 
-from .engine import DeviceEngine, HaltReason
+from .engine import DeviceEngine, HaltReason, RecordLevel
 from .generators import SYNTH_DEGREE, SYNTH_SEED, SystemArrays
 from .matrices import Format, NeuronRuleMap, RuleVector
 from .selection import FirstApplicable, Selection, mix64_array
@@ -119,6 +119,20 @@ def decide_halt(flags: np.ndarray, last: bool = False) -> HaltReason | str | Non
     return None
 
 
+def _record_flags(record: RecordLevel | None) -> int:
+    """RecordLevel -> SNP_REC_* flags (None / no recording: 0)."""
+    if record is None:
+        return 0
+    return {RecordLevel.CONFIGS: nat.SNP_REC_CONFIGS,
+            RecordLevel.CONFIGS_AND_DELAYS: nat.SNP_REC_CONFIGS | nat.SNP_REC_DELAYS,
+            RecordLevel.FULL: nat.SNP_REC_CONFIGS | nat.SNP_REC_DELAYS | nat.SNP_REC_SPIKING}[RecordLevel(record)]
+
+
+def rule_base(arrays: SystemArrays, layout: ShardLayout, rank: int) -> int:
+    """Global id of rank ``rank``'s first rule (its local rule r is global r + base)."""
+    return int(arrays.rule_map.offsets[layout.bounds(rank)[0]])
+
+
 def local_arrays(arrays: SystemArrays, layout: ShardLayout, rank: int) -> SystemArrays:
     """Slice a whole-system SystemArrays to rank ``rank``'s node arrays (the
     adjacency stays global: the engine keeps the edges entering its rows)."""
@@ -149,7 +163,11 @@ class ShardedEngine:
     """
 
     def __init__(self, local: SystemArrays, q: int, rank: int, world: int, device: int = 0,
-                 variant: str = "tiled", p_span: tuple[int, int] | None = None):
+                 variant: str = "tiled", p_span: tuple[int, int] | None = None, rule_base: int = 0):
+        # rule_base: global id of this rank's first rule (recorded spiking rows
+        # carry global rule ids, sharded.rule_base)
+        self.rule_base = int(rule_base)
+        self.last_trace = None
         # p_span: the system-wide (pmin, pmax) of the produced amounts (see
         # global_p_range); every rank must pass the same one.  Default: this
         # rank's own rules (only safe when they span the whole system's range)
@@ -202,7 +220,7 @@ class ShardedEngine:
 
     def run(self, max_steps: int, exchange: Callable[[int], None] | None = None,
             selection: Selection = FirstApplicable(), poll_every: int = 8, collect_stats: bool = False,
-            barrier: Callable[[], None] | None = None):
+            barrier: Callable[[], None] | None = None, record: RecordLevel | None = None):
         """Step to halt.  All-gather mode: ``exchange(slot)`` must all-gather
         exchange slot ``slot`` across ranks after each launch (same call on
         every rank).  Peer-exchange mode (after ``connect_p2p``): no exchange;
@@ -214,7 +232,8 @@ class ShardedEngine:
             raise ValueError("all-gather mode needs an exchange callable")
         eng = self.engine
         eng.begin()
-        eng.configure(max_steps, selection, collect_stats)
+        flags = _record_flags(record)
+        eng.configure(max_steps, selection, collect_stats, record=flags)
         if barrier is not None:
             barrier()
         k = 0
@@ -231,6 +250,13 @@ class ShardedEngine:
         # poll() raised NegativeSpikes / NativeError for the other halts
         reason = {nat.SNP_HALT_STEP_LIMIT: HaltReason.STEP_LIMIT,
                   nat.SNP_HALT_NO_APPLICABLE: HaltReason.NO_APPLICABLE_RULES}[int(res.halt)]
+        self.last_trace = None
+        if flags:
+            steps = int(res.steps)
+            c, d, ch = eng.read_trace(steps + 1, steps, flags)
+            if ch is not None:  # this rank's rule indices -> the system's global rule ids
+                ch = np.where(ch >= 0, ch + self.rule_base, -1)
+            self.last_trace = (c, d, ch)
         return cfg, dly, int(res.steps), reason, res.stats_dict(), k
 
 

@@ -564,3 +564,46 @@ def test_partition_rank_without_rows_is_rejected():
     assert lay.bounds(1)[0] == lay.bounds(1)[1]
     with pytest.raises(ValueError, match="owns no neurons"):
         shd.ShardedEngine(shd.local_arrays(a, lay, 1), 100, 1, 2, p_span=shd.p_range(a.rules))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_partition_records_full_traces(world):
+    """Recording in row-partitioned runs: every rank keeps its rows of the
+    FULL trace on the device (snp_configure with record flags, snp_read_trace);
+    the ranks' columns side by side are the single engine's trace, with the
+    chosen rules as global ids."""
+    from oracle.snp_oracle import trace_digest
+    arrays = snp.synth_v1(40_000, with_delays=True)
+    sel = snp.SeededRandom(11)
+    L = 9
+    want = snp.simulate_prepared(snp.prepare(arrays, snp.Format.COMPRESSED),
+                                 snp.SimOptions(max_steps=L, selection=sel, record=snp.RecordLevel.FULL))
+    q = arrays.neuron_count
+    lay = shd.shard_layout(q, world)
+    span = shd.p_range(arrays.rules)
+    ranks = [shd.ShardedEngine(shd.local_arrays(arrays, lay, r), q, r, world, p_span=span,
+                               rule_base=shd.rule_base(arrays, lay, r)) for r in range(world)]
+    shd.ShardedEngine.connect_local(ranks)
+    stream = torch.cuda.Stream()
+    flags = shd._record_flags(snp.RecordLevel.FULL)
+    for r in ranks:
+        r.engine.set_stream(stream.cuda_stream)
+        r.engine.begin()
+        r.engine.configure(L, sel, record=flags)
+    k = 0
+    while True:
+        for r in ranks:
+            r.engine.launch_step()
+        k += 1
+        res = [r.engine.poll() for r in ranks]
+        if res[0].halt != 0:
+            break
+        assert k <= L + 3
+    steps = int(res[0].steps)
+    assert steps == want.steps
+    parts = [r.engine.read_trace(steps + 1, steps, flags) for r in ranks]
+    cfg = np.concatenate([p[0] for p in parts], axis=1)
+    dly = np.concatenate([p[1] for p in parts], axis=1)
+    ch = np.concatenate([np.where(p[2] >= 0, p[2] + r.rule_base, -1) for p, r in zip(parts, ranks)], axis=1)
+    assert trace_digest(list(cfg), list(dly), list(ch)) == trace_digest(want.configs, want.delays, want.spiking)
