@@ -9,7 +9,7 @@ Reference: ``pkg/src/snpsim/selection.py``.
   neuron) mod 2**64 (selection.py:37-45)
 
 The simulation itself never calls these Python helpers: the B200 kernels
-evaluate the same hash on device (``csrc/snp_kernels.cuh``, ``mix64``).
+evaluate the same hash on device (``csrc/snp_device.cuh``, ``mix64``).
 They are kept because the reference exports them and its tests pin the
 vectorised form against the scalar one (test_engine.py:52-58).
 """
