@@ -2307,7 +2307,13 @@ int snp_configure(snp_engine* e, const snp_run_opts* o) {
     // recording (row partitions, snp_read_trace): every row of the run stays
     // in the device ring -- step k's rows at slot k (trace_base 0)
     const int rec = o->record & (SNP_REC_CONFIGS | SNP_REC_DELAYS | SNP_REC_SPIKING);
-    if (rec) TRY(ensure_trace(e, o->max_steps + 2));
+    if (rec) {
+        const double bytes = ((double)o->max_steps + 2.0) * (double)std::max<long long>(1, e->q) * 16.0;
+        if (bytes > 64e9)
+            return fail(SNP_ERR_CAPACITY, "recording %lld steps of %lld neurons keeps %.1f GB of rows on the device",
+                        (long long)o->max_steps, e->q, bytes / 1e9);
+        TRY(ensure_trace(e, o->max_steps + 2));
+    }
     c.record = rec;
     c.stats_on = o->collect_stats ? 1 : 0;
     c.stop_at = 0x3fffffffffffffffll;
