@@ -331,14 +331,13 @@ int build_tiles(snp_engine* e, const snp_system_desc* d, const hvec<uint32_t>& s
         e->cbits = worst < 256 ? 8 : (worst < 65536 ? 16 : 32);
         if (const char* env = getenv("SNPB200_COUNTER_BITS")) e->cbits = std::max(e->cbits, atoi(env));
     }
-    // one CTA per SM; a multiple of the SM count in tiles keeps them balanced
-    // (2 tiles per SM with 16-bit counters still leaves a 3 x 48 KB ring;
-    // 4 per SM with 32-bit counters; measured on K3, profiles/r1_history.md)
-    long long per_sm = (e->cbits <= 16 && heavy.empty()) ? 2 : 4;  // heavy-rule systems: more, smaller tiles
-    // sources spread over >= 4x this engine's rows (row partition at 4+ ranks):
-    // each tile's P windows span all sources, so fewer, larger tiles read
-    // fewer window bytes per edge (large systems)
-    if (per_sm == 2 && !s.tp && n_src >= 4 * std::max<long long>(q, 1)) per_sm = 1;
+    // one CTA per SM; a multiple of the SM count in tiles keeps them balanced.
+    // 8/16-bit counters: one tile per SM (T = q / 148; the ring keeps at
+    // least 3 x 48 KB, T shrinks below if needed) -- measured on the round-2
+    // kernel: K3 0.240 -> 0.229 ms, K4 0.241 -> 0.229, 10^6 neurons 0.044 ->
+    // 0.040 vs two tiles per SM (profiles/r2_history.md); 32-bit counters and
+    // heavy-rule systems: 4 per SM (more, smaller tiles)
+    long long per_sm = (e->cbits <= 16 && heavy.empty()) ? 1 : 4;
     if (const char* env = getenv("SNPB200_TILES_PER_SM")) per_sm = std::max(1, atoi(env));
     long long T = ceil_div(std::max<long long>(q, 1), per_sm * n_sm);
     if (!heavy.empty()) T = std::min<long long>(T, std::max<long long>(32, 32ll * q / (long long)heavy.size()));
