@@ -518,8 +518,10 @@ def _nccl_worker(port, out):
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
                 ex = shd.torch_allgather_exchange(sh)
-                cfg, dly, steps, reason, _, launches = sh.run(L, exchange=ex)
-            res[case] = (cfg.tolist(), dly.tolist(), steps, str(reason), launches)
+                cfg, dly, steps, reason, _, launches = sh.run(L, exchange=ex, record=snp.RecordLevel.FULL)
+            tc, td, ts = sh.last_trace
+            res[case] = (cfg.tolist(), dly.tolist(), steps, str(reason), launches,
+                         (tc.tolist(), td.tolist(), ts.tolist()))
         out.put(res)
     finally:
         dist.destroy_process_group()
@@ -543,7 +545,8 @@ def test_nccl_allgather_exchange_runs():
     res = out.get(timeout=600)
     p.join(60)
     assert p.exitcode == 0
-    for case, (cfg, dly, steps, reason, launches) in res.items():
+    from oracle.snp_oracle import trace_digest
+    for case, (cfg, dly, steps, reason, launches, (tc, td, ts)) in res.items():
         if case == "sort":
             arrays, L = snp.sort_arrays(snp.SortInstance(200)), 300
         else:
@@ -552,6 +555,11 @@ def test_nccl_allgather_exchange_runs():
         assert cfg == want.config.tolist() and dly == want.delays.tolist(), case
         assert steps == want.steps and reason == str(want.halt_reason), case
         assert launches >= steps
+        full = snp.simulate_prepared(snp.prepare(arrays, snp.Format.COMPRESSED),
+                                     snp.SimOptions(max_steps=L, record=snp.RecordLevel.FULL))
+        got = [np.asarray(x, dtype=np.int64) for x in (tc, td, ts)]
+        assert trace_digest(list(got[0]), list(got[1]), list(got[2])) == \
+            trace_digest(full.configs, full.delays, full.spiking), case
 
 
 @pytest.mark.gpu
