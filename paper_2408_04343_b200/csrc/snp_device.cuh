@@ -2192,8 +2192,8 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const
 // possible flush, overflow = the in-degree sum (checked on every reservation).
 
 #ifndef SNP_BIN_THREADS
-#define SNP_BIN_THREADS 768  // 24 warps: 80 registers per thread (1024 threads leave 64, and the
-                             // delivery loop then rematerialises per-kernel constants -- ncu source view)
+#define SNP_BIN_THREADS 1024  // 32 warps (64 registers: no spills since the walks became separate
+                              // instances); same box: K3 ELL 1.022 (768) -> 0.948 ms, push 0.932 -> 0.857
 #endif
 constexpr int kBinThreads = SNP_BIN_THREADS;
 constexpr int kBinUnroll = 4;    // column chunks in flight per lane
