@@ -2198,7 +2198,7 @@ __global__ void __launch_bounds__(kBlock, kStepMinBlocks) push_step_kernel(const
 constexpr int kBinThreads = SNP_BIN_THREADS;
 constexpr int kBinUnroll = 4;    // column chunks in flight per lane
 #ifndef SNP_BIN_GUNROLL
-#define SNP_BIN_GUNROLL 6
+#define SNP_BIN_GUNROLL 4
 #endif
 constexpr int kBinGUnroll = SNP_BIN_GUNROLL;  // ELL column-group passes in flight per warp
 
