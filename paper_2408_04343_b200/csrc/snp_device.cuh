@@ -2212,8 +2212,14 @@ struct BinEntry {
 template <>
 struct BinEntry<true> {
     using T = uint16_t;
-    static constexpr int kCap = 256;
-    static constexpr int kWin = 4;
+#ifndef SNP_BIN_CAP
+#define SNP_BIN_CAP 256
+#endif
+    static constexpr int kCap = SNP_BIN_CAP;
+#ifndef SNP_BIN_WIN
+#define SNP_BIN_WIN 4
+#endif
+    static constexpr int kWin = SNP_BIN_WIN;
     static constexpr int kVec = 8;
 };
 // flushes per step into one tile are at most ceil(q / (kBinThreads * kWin)) + ntiles
